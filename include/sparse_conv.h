@@ -1,0 +1,166 @@
+/*
+ * sparse_conv.h -- C ABI of libsparseconv.so, a B200 (sm_100a) implementation
+ * of the ReLU-sparse forward convolution of Shi & Chu, arXiv 1704.07724
+ * ("Speeding up Convolutional Neural Networks By Exploiting the Sparsity of
+ * Rectifier Units", /root/reference/PAPER.md, cited as P:<line>).
+ *
+ * What is computed (Sec. 3 Eq. 1, with Table 1's padding P and
+ * stride T, and the batch/bias/groups readings R2-R4 of DESIGN.md):
+ *
+ *   out[n,k,y,x] = bias[k] + sum_{c in group(k)} sum_{r<R} sum_{t<S}
+ *                  in[n, c, y*T + r - P, x*T + t - P] * W[k, c - g*C/G, r, t]
+ *
+ * with out-of-range input reads equal to zero (virtual padding) and
+ * H_out = floor((H + 2P - R)/T) + 1 (reading R1; P:37 is garbled).
+ *
+ * sparse_conv_forward skips every multiply-add whose input is zero (the
+ * "inverse sparse convolution" of P:119-123) in two stages: (1) a compaction
+ * kernel emits per-(image, channel, row-tile) nonzero lists (ISC step 1,
+ * P:123); (2) an output-stationary gather kernel accumulates
+ * sum_{nonzeros} v * W (ISC steps 2-3).  dense_conv_forward is the
+ * GEMM-mapped dense convolution of P:109-117 (Fig. 2) on tcgen05 tensor cores
+ * (TF32 inputs, fp32 accumulation) -- the in-library comparison.
+ *
+ * Conventions (all functions):
+ *  - Tensors are fp32, contiguous NCHW (input/output) and [K][C/G][R][S]
+ *    (weights).  Device pointers must be 16-byte aligned and belong to the
+ *    plan's device; otherwise SC_ERR_INVALID_ARGUMENT.
+ *  - Errors never abort; sc_last_error() returns a thread-local detail string.
+ *  - Every element count must be < 2^31, else SC_ERR_UNSUPPORTED.
+ *  - Inputs are expected to be finite (ReLU outputs).  Non-finite inputs are
+ *    outside the sparse path's contract (reading R7).
+ */
+#ifndef SPARSE_CONV_H_
+#define SPARSE_CONV_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without including cuda_runtime.h */
+typedef struct CUstream_st *sc_stream_t;
+
+typedef enum {
+    SC_OK = 0,
+    SC_ERR_INVALID_ARGUMENT = 1, /* null/misaligned/wrong-device pointer, bad n */
+    SC_ERR_SHAPE = 2,            /* parameters violate the shape rules below    */
+    SC_ERR_UNSUPPORTED = 3,      /* valid but not implemented (e.g. >= 2^31)    */
+    SC_ERR_CUDA = 4,             /* a CUDA call failed; see sc_last_error()     */
+    SC_ERR_OUT_OF_MEMORY = 5
+} sc_status;
+
+/* Paper Table 1 plus batch and groups.
+ * Shape rules (SC_ERR_SHAPE otherwise): n,c,h,w,k,r,s,stride,groups >= 1;
+ * pad >= 0; r <= h + 2*pad; s <= w + 2*pad; groups divides c and k. */
+typedef struct {
+    int64_t n, c, h, w;   /* input NCHW; n = the largest batch this plan serves */
+    int64_t k, r, s;      /* K filters of R x S; weight [K][C/groups][R][S]     */
+    int64_t stride;       /* T, same in both dimensions                  */
+    int64_t pad;          /* P, symmetric zero padding                   */
+    int64_t groups;       /* grouped convolution (reading R4)                   */
+    uint32_t flags;       /* 0 or SC_FLAG_FUSE_RELU                             */
+} sc_conv_params;
+
+/* Apply Z = max(0, O) (Eq. 2) in the epilogue of both forward paths. */
+#define SC_FLAG_FUSE_RELU 1u
+
+typedef struct sc_plan_s *sc_plan;
+
+/* Read-only view of the stage-1 workspace (device pointers owned by the plan).
+ * List format (reading R9): list id = (n*C + c)*tiles_per_plane + tile; a list
+ * covers rows [tile*row_tile_h, min(H,(tile+1)*row_tile_h)) of plane (n,c);
+ * entry e < counts[id] holds values[id*slot_capacity + e] (bit copy of an
+ * input x with x != 0.0f) and idx[id*slot_capacity + e] = (row - tile*TH)*W +
+ * col as u8 (idx_bytes 1) or u16 (idx_bytes 2), ascending.  Slots beyond the
+ * count are undefined. */
+typedef struct {
+    const float *values;
+    const void *idx;
+    const uint32_t *counts;
+    int64_t num_lists;
+    int64_t slot_capacity;
+    int64_t tiles_per_plane;
+    int32_t row_tile_h;
+    int32_t idx_bytes;
+} sc_lists_view;
+
+/* Output shape (N = params.n): out_nchw = {n, k, H_out, W_out}.  Pure host
+ * function; SC_ERR_SHAPE on invalid params. */
+sc_status sparse_conv_output_shape(const sc_conv_params *params, int64_t out_nchw[4]);
+
+/* Create a plan on `device`: validates params, allocates plan-owned device
+ * memory (packed weights in the K-contiguous layout of ISC step 2; the
+ * dense path's TF32 operand; bias; the stage-1 list workspace for params.n
+ * images), packs the weights and synchronizes.  d_weight [K][C/G][R][S] and
+ * d_bias [K] (NULL = zero bias) are device pointers that the caller may free
+ * when this returns.  *out_plan is NULL on failure. */
+sc_status sparse_conv_create(const sc_conv_params *params, const float *d_weight,
+                             const float *d_bias, int device, sc_plan *out_plan);
+
+/* The hot path: out = conv(in) skipping zero inputs (stages 1 and 2) for the
+ * first n (1 <= n <= params.n) images.  d_in [n][C][H][W], d_out
+ * [n][K][H_out][W_out] are caller-owned device buffers; d_out is fully
+ * overwritten.  Stream-ordered and asynchronous: no allocation and no host
+ * synchronization, so it can be captured in a CUDA graph.  A plan must not run
+ * two forwards concurrently (the list workspace is shared).  Device faults
+ * surface at the caller's next synchronization. */
+sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *d_out,
+                              sc_stream_t stream);
+
+/* Dense comparison path: implicit GEMM on tcgen05 tensor cores,
+ * operands rounded to TF32 (cvt.rna), fp32 accumulation.  Same buffer and
+ * stream contract as sparse_conv_forward. */
+sc_status dense_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *d_out,
+                             sc_stream_t stream);
+
+/* End-to-end variant of sparse_conv_forward with HOST buffers: copies h_in
+ * (n images) to plan-owned device staging, runs the sparse forward, copies the
+ * result back into h_out, all on `stream`, then synchronizes the stream.  For
+ * full copy bandwidth h_in/h_out should be pinned (cudaHostAlloc/register). */
+sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, float *h_out,
+                                   sc_stream_t stream);
+
+/* Free everything the plan owns.  NULL is a no-op. */
+sc_status sparse_conv_destroy(sc_plan plan);
+
+/* Static description of a status code; never NULL. */
+const char *sc_status_string(sc_status status);
+/* Detail of the last error raised on this thread ("" if none). */
+const char *sc_last_error(void);
+
+/* ---- test and bench hooks ------------------------------------------------ */
+
+/* Stage 1 only (ISC step 1): fill the plan's list workspace from d_in. */
+sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float *d_in, sc_stream_t stream);
+
+/* Stage 2 only: the gather convolution from the lists already in the plan's
+ * workspace (produced by sparse_conv_compact for the same n). */
+sc_status sparse_conv_gather(sc_plan plan, int64_t n, float *d_out, sc_stream_t stream);
+
+/* Describe the plan's list workspace (device pointers, layout). */
+sc_status sparse_conv_lists(sc_plan plan, sc_lists_view *out);
+
+/* Which stage-2 kernel this plan launches: 0 = generic gather kernel (any
+ * stride/shape), >0 = a shape-specialised register-tile kernel variant id. */
+sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t *variant, const char **name);
+
+/* Number of kernels one sparse_conv_forward / dense_conv_forward launches. */
+sc_status sparse_conv_launch_count(sc_plan plan, int32_t *sparse_launches, int32_t *dense_launches);
+
+/* Micro-probes for the roofline denominators (bench only).  Each runs on the
+ * current device and stream 0 and synchronizes.
+ *   kind 0: FFMA  (3-register form) lanes-FMA per SM-clock
+ *   kind 1: FFMA2 (f32x2 with a broadcast scalar) lane-FMAs per SM-clock
+ * Returns the measured rate in *fma_per_clk_per_sm (clock64 based). */
+sc_status sc_probe_fma(int32_t kind, double *fma_per_clk_per_sm);
+
+/* Overwrite `bytes` of device scratch (>= 2x L2) to evict the L2 cache. */
+sc_status sc_flush_l2(void *d_scratch, size_t bytes, sc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSE_CONV_H_ */

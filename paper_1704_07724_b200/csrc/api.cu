@@ -1,0 +1,350 @@
+// C ABI of libsparseconv.so (include/sparse_conv.h): validation, plan
+// lifetime, launch sequencing.  No computation happens on the host.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "sc_internal.h"
+
+using sc::DenseGeom;
+using sc::Geometry;
+
+struct sc_plan_s {
+    sc_conv_params params;
+    int device;
+    Geometry g;
+    DenseGeom dg;
+    float* wpack = nullptr;    // [G][Cg][R][S][Kg_pad]
+    float* wdense = nullptr;   // [G][m_pad][kdim_pad], TF32-rounded (dense path)
+    float* bias = nullptr;     // [K]
+    float* values = nullptr;   // [num_lists][cap]
+    void* idx = nullptr;       // [num_lists][cap] u8/u16
+    uint32_t* counts = nullptr;
+    int variant = 0;
+    const char* variant_name = "generic";
+    // staging for sparse_conv_forward_host (allocated on first use)
+    float* stage_in = nullptr;
+    float* stage_out = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sc_status fail(sc_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+sc_status fail(sc_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+sc_status cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(SC_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    return fail(SC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int64_t kMaxElems = (int64_t(1) << 31) - 1;
+
+sc_status validate_params(const sc_conv_params* p) {
+    if (!p) return fail(SC_ERR_INVALID_ARGUMENT, "params is NULL");
+    if (p->n < 1 || p->c < 1 || p->h < 1 || p->w < 1 || p->k < 1 || p->r < 1 || p->s < 1 ||
+        p->stride < 1 || p->groups < 1)
+        return fail(SC_ERR_SHAPE, "extents, stride and groups must be >= 1");
+    if (p->pad < 0) return fail(SC_ERR_SHAPE, "pad must be >= 0");
+    if (p->r > p->h + 2 * p->pad || p->s > p->w + 2 * p->pad)
+        return fail(SC_ERR_SHAPE, "kernel %lldx%lld larger than padded input", (long long)p->r, (long long)p->s);
+    if (p->c % p->groups || p->k % p->groups) return fail(SC_ERR_SHAPE, "groups must divide C and K");
+    if (p->flags & ~SC_FLAG_FUSE_RELU) return fail(SC_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", p->flags);
+    return SC_OK;
+}
+
+// Reading R9: list format.
+void list_format(int64_t H, int64_t W, int64_t* th, int64_t* tiles, int64_t* idx_bytes, int64_t* cap) {
+    *th = (H * W <= 256) ? H : ((256 / W) > 1 ? 256 / W : 1);
+    *idx_bytes = (*th * W <= 256) ? 1 : 2;
+    *cap = (*th * W + 15) / 16 * 16;
+    *tiles = (H + *th - 1) / *th;
+}
+
+sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg) {
+    g->N = p->n; g->C = p->c; g->H = p->h; g->W = p->w; g->K = p->k; g->R = p->r; g->S = p->s;
+    g->T = p->stride; g->P = p->pad; g->G = p->groups;
+    g->Ho = (p->h + 2 * p->pad - p->r) / p->stride + 1;
+    g->Wo = (p->w + 2 * p->pad - p->s) / p->stride + 1;
+    g->Cg = p->c / p->groups;
+    g->Kg = p->k / p->groups;
+    g->Kg_pad = (g->Kg + 31) / 32 * 32;
+    g->kblocks = g->Kg_pad / 32;
+    g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
+    list_format(g->H, g->W, &g->th, &g->tiles, &g->idx_bytes, &g->cap);
+    g->num_lists = g->N * g->C * g->tiles;
+    dg->kdim = g->Cg * g->R * g->S;
+    dg->kdim_pad = (dg->kdim + 31) / 32 * 32;
+    dg->m_pad = (g->Kg + 127) / 128 * 128;
+    const int64_t in_e = g->N * g->C * g->H * g->W, out_e = g->N * g->K * g->Ho * g->Wo;
+    const int64_t w_e = g->G * g->Cg * g->R * g->S * g->Kg_pad;
+    const int64_t l_e = g->num_lists * g->cap;
+    const int64_t d_e = g->G * dg->m_pad * dg->kdim_pad;
+    if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || l_e > kMaxElems || d_e > kMaxElems)
+        return fail(SC_ERR_UNSUPPORTED, "a tensor has >= 2^31 elements");
+    return SC_OK;
+}
+
+sc_status check_dev_ptr(const sc_plan_s* plan, const void* ptr, const char* name) {
+    if (!ptr) return fail(SC_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+    if (reinterpret_cast<uintptr_t>(ptr) % 16)
+        return fail(SC_ERR_INVALID_ARGUMENT, "%s is not 16-byte aligned", name);
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SC_ERR_INVALID_ARGUMENT, "%s: not a CUDA pointer (%s)", name, cudaGetErrorString(e));
+    }
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+        return fail(SC_ERR_INVALID_ARGUMENT, "%s is not device memory", name);
+    if (attr.device != plan->device)
+        return fail(SC_ERR_INVALID_ARGUMENT, "%s is on device %d, plan is on device %d", name, attr.device,
+                    plan->device);
+    return SC_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void free_plan(sc_plan_s* p) {
+    cudaFree(p->wpack);
+    cudaFree(p->wdense);
+    cudaFree(p->bias);
+    cudaFree(p->values);
+    cudaFree(p->idx);
+    cudaFree(p->counts);
+    cudaFree(p->stage_in);
+    cudaFree(p->stage_out);
+    delete p;
+}
+
+sc_status check_forward(sc_plan plan, int64_t n) {
+    if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (n < 1 || n > plan->params.n)
+        return fail(SC_ERR_INVALID_ARGUMENT, "n=%lld outside [1, %lld]", (long long)n, (long long)plan->params.n);
+    return SC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sc_status_string(sc_status s) {
+    switch (s) {
+        case SC_OK: return "ok";
+        case SC_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case SC_ERR_SHAPE: return "invalid shape";
+        case SC_ERR_UNSUPPORTED: return "unsupported";
+        case SC_ERR_CUDA: return "CUDA error";
+        case SC_ERR_OUT_OF_MEMORY: return "out of memory";
+    }
+    return "unknown status";
+}
+
+const char* sc_last_error(void) { return g_last_error.c_str(); }
+
+sc_status sparse_conv_output_shape(const sc_conv_params* params, int64_t out_nchw[4]) {
+    sc_status st = validate_params(params);
+    if (st != SC_OK) return st;
+    if (!out_nchw) return fail(SC_ERR_INVALID_ARGUMENT, "out_nchw is NULL");
+    out_nchw[0] = params->n;
+    out_nchw[1] = params->k;
+    out_nchw[2] = (params->h + 2 * params->pad - params->r) / params->stride + 1;
+    out_nchw[3] = (params->w + 2 * params->pad - params->s) / params->stride + 1;
+    return SC_OK;
+}
+
+sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight, const float* d_bias, int device,
+                             sc_plan* out_plan) {
+    if (!out_plan) return fail(SC_ERR_INVALID_ARGUMENT, "out_plan is NULL");
+    *out_plan = nullptr;
+    sc_status st = validate_params(params);
+    if (st != SC_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return fail(SC_ERR_INVALID_ARGUMENT, "device %d not available (%d devices)", device, ndev);
+    }
+    sc_plan_s* plan = new (std::nothrow) sc_plan_s();
+    if (!plan) return fail(SC_ERR_OUT_OF_MEMORY, "host allocation failed");
+    plan->params = *params;
+    plan->device = device;
+    if ((st = make_geometry(params, &plan->g, &plan->dg)) != SC_OK) {
+        delete plan;
+        return st;
+    }
+    DeviceGuard guard(device);
+    if ((st = check_dev_ptr(plan, d_weight, "d_weight")) != SC_OK ||
+        (d_bias && (st = check_dev_ptr(plan, d_bias, "d_bias")) != SC_OK)) {
+        delete plan;
+        return st;
+    }
+    const Geometry& g = plan->g;
+    const DenseGeom& dg = plan->dg;
+    cudaError_t e;
+    const size_t wbytes = sizeof(float) * g.G * g.Cg * g.R * g.S * g.Kg_pad;
+    const size_t dbytes = sizeof(float) * g.G * dg.m_pad * dg.kdim_pad;
+    if ((e = cudaMalloc(&plan->wpack, wbytes)) != cudaSuccess ||
+        (e = cudaMalloc(&plan->wdense, dbytes)) != cudaSuccess ||
+        (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
+        (e = cudaMalloc(&plan->values, sizeof(float) * g.num_lists * g.cap)) != cudaSuccess ||
+        (e = cudaMalloc(&plan->idx, (size_t)g.idx_bytes * g.num_lists * g.cap)) != cudaSuccess ||
+        (e = cudaMalloc(&plan->counts, sizeof(uint32_t) * g.num_lists)) != cudaSuccess) {
+        free_plan(plan);
+        return cuda_fail(e, "sparse_conv_create: cudaMalloc");
+    }
+    cudaStream_t st0 = 0;
+    if (d_bias)
+        e = cudaMemcpyAsync(plan->bias, d_bias, sizeof(float) * g.K, cudaMemcpyDeviceToDevice, st0);
+    else
+        e = cudaMemsetAsync(plan->bias, 0, sizeof(float) * g.K, st0);
+    if (e == cudaSuccess) e = sc::launch_pack_weights(g, d_weight, plan->wpack, st0);
+    if (e == cudaSuccess) e = sc::launch_pack_dense(g, dg, d_weight, plan->wdense, st0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st0);
+    if (e != cudaSuccess) {
+        free_plan(plan);
+        return cuda_fail(e, "sparse_conv_create: pack");
+    }
+    const char* name = nullptr;
+    plan->variant = sc::gather_fast_select(g, &name);
+    plan->variant_name = plan->variant ? name : "generic";
+    *out_plan = plan;
+    return SC_OK;
+}
+
+sc_status sparse_conv_destroy(sc_plan plan) {
+    if (!plan) return SC_OK;
+    DeviceGuard guard(plan->device);
+    free_plan(plan);
+    return SC_OK;
+}
+
+sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float* d_in, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
+    DeviceGuard guard(plan->device);
+    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->values, plan->idx, plan->counts,
+                                       (cudaStream_t)stream);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "compact launch");
+}
+
+sc_status sparse_conv_gather(sc_plan plan, int64_t n, float* d_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
+    DeviceGuard guard(plan->device);
+    cudaError_t e;
+    if (plan->variant > 0)
+        e = sc::launch_gather_fast(plan->variant, plan->g, n, plan->values, plan->idx, plan->counts, plan->wpack,
+                                   plan->bias, d_out, (cudaStream_t)stream);
+    else
+        e = sc::launch_gather_generic(plan->g, n, plan->values, plan->idx, plan->counts, plan->wpack, plan->bias,
+                                      d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "gather launch");
+}
+
+sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float* d_in, float* d_out, sc_stream_t stream) {
+    sc_status st = sparse_conv_compact(plan, n, d_in, stream);
+    if (st != SC_OK) return st;
+    return sparse_conv_gather(plan, n, d_out, stream);
+}
+
+sc_status dense_conv_forward(sc_plan plan, int64_t n, const float* d_in, float* d_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
+    DeviceGuard guard(plan->device);
+    cudaError_t e = sc::launch_dense_tc(plan->g, plan->dg, n, d_in, plan->wdense, plan->bias, d_out,
+                                        (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) return fail(SC_ERR_UNSUPPORTED, "dense path: shape not supported");
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "dense launch");
+}
+
+sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, float* h_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if (!h_in || !h_out) return fail(SC_ERR_INVALID_ARGUMENT, "host buffer is NULL");
+    DeviceGuard guard(plan->device);
+    const Geometry& g = plan->g;
+    const size_t in_b = sizeof(float) * g.N * g.C * g.H * g.W, out_b = sizeof(float) * g.N * g.K * g.Ho * g.Wo;
+    cudaError_t e;
+    if (!plan->stage_in) {
+        if ((e = cudaMalloc(&plan->stage_in, in_b)) != cudaSuccess) return cuda_fail(e, "staging alloc");
+        if ((e = cudaMalloc(&plan->stage_out, out_b)) != cudaSuccess) return cuda_fail(e, "staging alloc");
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nin = sizeof(float) * n * g.C * g.H * g.W, nout = sizeof(float) * n * g.K * g.Ho * g.Wo;
+    if ((e = cudaMemcpyAsync(plan->stage_in, h_in, nin, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "H2D copy");
+    if ((st = sparse_conv_forward(plan, n, plan->stage_in, plan->stage_out, stream)) != SC_OK) return st;
+    if ((e = cudaMemcpyAsync(h_out, plan->stage_out, nout, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "D2H copy");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+    return SC_OK;
+}
+
+sc_status sparse_conv_lists(sc_plan plan, sc_lists_view* out) {
+    if (!plan || !out) return fail(SC_ERR_INVALID_ARGUMENT, "NULL argument");
+    out->values = plan->values;
+    out->idx = plan->idx;
+    out->counts = plan->counts;
+    out->num_lists = plan->g.num_lists;
+    out->slot_capacity = plan->g.cap;
+    out->tiles_per_plane = plan->g.tiles;
+    out->row_tile_h = (int32_t)plan->g.th;
+    out->idx_bytes = (int32_t)plan->g.idx_bytes;
+    return SC_OK;
+}
+
+sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t* variant, const char** name) {
+    if (!plan || !variant) return fail(SC_ERR_INVALID_ARGUMENT, "NULL argument");
+    *variant = plan->variant;
+    if (name) *name = plan->variant_name;
+    return SC_OK;
+}
+
+sc_status sparse_conv_launch_count(sc_plan plan, int32_t* sparse_launches, int32_t* dense_launches) {
+    if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (sparse_launches) *sparse_launches = 2;
+    if (dense_launches) *dense_launches = 1;
+    return SC_OK;
+}
+
+sc_status sc_probe_fma(int32_t kind, double* fma_per_clk_per_sm) {
+    if (!fma_per_clk_per_sm || kind < 0 || kind > 2) return fail(SC_ERR_INVALID_ARGUMENT, "bad probe arguments");
+    cudaError_t e = sc::probe_fma(kind, fma_per_clk_per_sm);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "fma probe");
+}
+
+sc_status sc_flush_l2(void* d_scratch, size_t bytes, sc_stream_t stream) {
+    if (!d_scratch || bytes < 16) return fail(SC_ERR_INVALID_ARGUMENT, "bad scratch");
+    cudaError_t e = sc::launch_flush(d_scratch, bytes, (cudaStream_t)stream);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "flush");
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+"""Thin ctypes binding of libsparseconv.so (include/sparse_conv.h).
+
+Argument marshalling only: every step of the convolution runs in the CUDA
+kernels of the library.  PyTorch provides device memory and streams.  There
+is no CPU fallback: if the library is missing or a call fails, this raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparseconv.so")
+
+SC_FLAG_FUSE_RELU = 1
+STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_SHAPE", 3: "SC_ERR_UNSUPPORTED",
+          4: "SC_ERR_CUDA", 5: "SC_ERR_OUT_OF_MEMORY"}
+
+# every symbol include/sparse_conv.h declares
+EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forward", "dense_conv_forward",
+           "sparse_conv_forward_host", "sparse_conv_destroy", "sc_status_string", "sc_last_error",
+           "sparse_conv_compact", "sparse_conv_gather", "sparse_conv_lists", "sparse_conv_kernel_variant",
+           "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2")
+
+
+class SparseConvError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ConvParams(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ("n", "c", "h", "w", "k", "r", "s", "stride", "pad", "groups")] + [
+        ("flags", ctypes.c_uint32)]
+
+
+class ListsView(ctypes.Structure):
+    _fields_ = [("values", ctypes.c_void_p), ("idx", ctypes.c_void_p), ("counts", ctypes.c_void_p),
+                ("num_lists", ctypes.c_int64), ("slot_capacity", ctypes.c_int64),
+                ("tiles_per_plane", ctypes.c_int64), ("row_tile_h", ctypes.c_int32), ("idx_bytes", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsparseconv.so.  Raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with "
+                               "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.sparse_conv_output_shape.argtypes = [ctypes.POINTER(ConvParams), ctypes.POINTER(ctypes.c_int64)]
+        L.sparse_conv_create.argtypes = [ctypes.POINTER(ConvParams), vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
+        for fn in ("sparse_conv_forward", "dense_conv_forward", "sparse_conv_forward_host"):
+            getattr(L, fn).argtypes = [vp, i64, vp, vp, vp]
+        L.sparse_conv_compact.argtypes = [vp, i64, vp, vp]
+        L.sparse_conv_gather.argtypes = [vp, i64, vp, vp]
+        L.sparse_conv_destroy.argtypes = [vp]
+        L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
+        L.sparse_conv_kernel_variant.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_char_p)]
+        L.sparse_conv_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+        L.sc_probe_fma.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+        L.sc_flush_l2.argtypes = [vp, ctypes.c_size_t, vp]
+        L.sc_status_string.argtypes = [st]
+        L.sc_status_string.restype = ctypes.c_char_p
+        L.sc_last_error.restype = ctypes.c_char_p
+        for fn in EXPORTS:
+            if fn not in ("sc_status_string", "sc_last_error"):
+                getattr(L, fn).restype = st
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        raise SparseConvError(status, lib().sc_last_error().decode())
+
+
+def _stream_handle(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_tensor(t, name, device, shape=None):
+    if not isinstance(t, torch.Tensor) or t.device != device or t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 tensor on {device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+class _DevArray:
+    """__cuda_array_interface__ wrapper so torch can view plan-owned memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, True),
+                                         "version": 3, "strides": None}
+
+
+def output_shape(n, c, h, w, k, r, s, stride=1, pad=0, groups=1):
+    p = ConvParams(n, c, h, w, k, r, s, stride, pad, groups, 0)
+    out = (ctypes.c_int64 * 4)()
+    _check(lib().sparse_conv_output_shape(ctypes.byref(p), out))
+    return tuple(out)
+
+
+class SparseConv:
+    """One convolution layer: plan-owned packed weights + list workspace.
+
+    weight: [K][C/groups][R][S] float32 CUDA tensor; bias: [K] or None.
+    max_batch: the largest n any forward will be called with."""
+
+    def __init__(self, weight, bias, max_batch, c, h, w, stride=1, pad=0, groups=1, fuse_relu=False):
+        device = weight.device
+        if device.type != "cuda":
+            raise ValueError("weight must be a CUDA tensor (there is no CPU path)")
+        k, cg, r, s = weight.shape
+        _check_tensor(weight, "weight", device)
+        if bias is not None:
+            _check_tensor(bias, "bias", device, (k,))
+        self.device = device
+        self.params = ConvParams(max_batch, c, h, w, k, r, s, stride, pad, groups,
+                                 SC_FLAG_FUSE_RELU if fuse_relu else 0)
+        self.in_shape = (c, h, w)
+        self.out_shape = output_shape(max_batch, c, h, w, k, r, s, stride, pad, groups)[1:]
+        self._plan = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _check(lib().sparse_conv_create(ctypes.byref(self.params), ctypes.c_void_p(weight.data_ptr()),
+                                            ctypes.c_void_p(bias.data_ptr()) if bias is not None else None,
+                                            device.index if device.index is not None else torch.cuda.current_device(),
+                                            ctypes.byref(self._plan)))
+
+    # -- hot path ---------------------------------------------------------
+    def forward(self, x, out=None, stream=None):
+        n = x.shape[0]
+        _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+        if out is None:
+            out = torch.empty((n,) + self.out_shape, device=self.device, dtype=torch.float32)
+        _check_tensor(out, "out", self.device, (n,) + self.out_shape)
+        _check(lib().sparse_conv_forward(self._plan, n, ctypes.c_void_p(x.data_ptr()),
+                                         ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    __call__ = forward
+
+    def dense_forward(self, x, out=None, stream=None):
+        n = x.shape[0]
+        _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+        if out is None:
+            out = torch.empty((n,) + self.out_shape, device=self.device, dtype=torch.float32)
+        _check_tensor(out, "out", self.device, (n,) + self.out_shape)
+        _check(lib().dense_conv_forward(self._plan, n, ctypes.c_void_p(x.data_ptr()),
+                                        ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def forward_host(self, h_in, h_out, stream=None):
+        """End-to-end call with HOST (ideally pinned) CPU tensors."""
+        n = h_in.shape[0]
+        for t, nm, shp in ((h_in, "h_in", (n,) + self.in_shape), (h_out, "h_out", (n,) + self.out_shape)):
+            if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or tuple(t.shape) != shp:
+                raise ValueError(f"{nm} must be a contiguous float32 CPU tensor of shape {shp}")
+        _check(lib().sparse_conv_forward_host(self._plan, n, ctypes.c_void_p(h_in.data_ptr()),
+                                              ctypes.c_void_p(h_out.data_ptr()), _stream_handle(stream)))
+        return h_out
+
+    # -- test hooks --------------------------------------------------------
+    def compact(self, x, stream=None):
+        n = x.shape[0]
+        _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+        _check(lib().sparse_conv_compact(self._plan, n, ctypes.c_void_p(x.data_ptr()), _stream_handle(stream)))
+
+    def gather(self, n, out=None, stream=None):
+        if out is None:
+            out = torch.empty((n,) + self.out_shape, device=self.device, dtype=torch.float32)
+        _check(lib().sparse_conv_gather(self._plan, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def lists(self, n):
+        """Device views of the list workspace for the first n images:
+        dict(values [L][cap] f32, idx [L][cap] u8/u16, counts [L] i32-view of u32, th, tiles, cap)."""
+        v = ListsView()
+        _check(lib().sparse_conv_lists(self._plan, ctypes.byref(v)))
+        nl = n * self.in_shape[0] * v.tiles_per_plane
+        cap = v.slot_capacity
+        with torch.cuda.device(self.device):
+            values = torch.as_tensor(_DevArray(v.values, (nl, cap), "<f4"), device=self.device)
+            idx = torch.as_tensor(_DevArray(v.idx, (nl, cap), "|u1" if v.idx_bytes == 1 else "<i2"),
+                                  device=self.device)
+            counts = torch.as_tensor(_DevArray(v.counts, (nl,), "<i4"), device=self.device)
+        return dict(values=values, idx=idx, counts=counts, th=v.row_tile_h, tiles=v.tiles_per_plane, cap=cap,
+                    idx_bytes=v.idx_bytes)
+
+    @property
+    def variant(self):
+        vid, name = ctypes.c_int32(), ctypes.c_char_p()
+        _check(lib().sparse_conv_kernel_variant(self._plan, ctypes.byref(vid), ctypes.byref(name)))
+        return vid.value, name.value.decode()
+
+    @property
+    def launch_counts(self):
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().sparse_conv_launch_count(self._plan, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self._plan:
+            lib().sparse_conv_destroy(self._plan)
+            self._plan = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def probe_fma(kind):
+    """FP32 pipe probe: lane-FMAs retired per SM clock (kind 0 FFMA, 1 FFMA2, 2 FFMA2+int)."""
+    r = ctypes.c_double()
+    _check(lib().sc_probe_fma(kind, ctypes.byref(r)))
+    return r.value
+
+
+def flush_l2(scratch, stream=None):
+    _check(lib().sc_flush_l2(ctypes.c_void_p(scratch.data_ptr()), scratch.numel() * scratch.element_size(),
+                             _stream_handle(stream)))

@@ -1,0 +1,263 @@
+"""GPU parity of the sparse path (C-ABI library) against the CPU oracle.
+
+Bars (north star):
+* stage-1 lists bit-exact (counts, values bits, indices; slack never compared);
+* outputs within |gpu - oracle| <= 1e-5 * mass + 1e-6 per element;
+* integer-valued data: bit-exact (every partial sum is exact in fp32).
+Full BASELINE sizes run in the bench's launch configuration (same plan, full
+batch); the oracle then checks sampled images (images are independent,
+Eq. 1 has no cross-image term)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1704_07724_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def sc():
+    from paper_1704_07724_b200 import sparseconv
+    sparseconv.lib()
+    return sparseconv
+
+
+def make_conv(sc, shp, w, b, relu=False, max_batch=None):
+    return sc.SparseConv(torch.from_numpy(w).to(DEV), None if b is None else torch.from_numpy(b).to(DEV),
+                         max_batch or shp.n, shp.c, shp.h, shp.w, shp.stride, shp.pad, shp.groups, fuse_relu=relu)
+
+
+def check_lists(conv, x, n):
+    """Bit-exact comparison of the GPU list workspace with oracle.compact."""
+    ref = oracle.compact(x[:n])
+    got = conv.lists(n)
+    assert got["th"] == ref["th"] and got["tiles"] == ref["tiles"] and got["cap"] == ref["cap"]
+    counts = got["counts"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(counts, ref["counts"])
+    cap = ref["cap"]
+    valid = np.arange(cap)[None, :] < ref["counts"][:, None]
+    gv = got["values"].cpu().numpy().view(np.uint32)
+    gi = got["idx"].cpu().numpy().view(ref["idx"].dtype)
+    assert np.array_equal(np.where(valid, gv, 0), np.where(valid, ref["values"].view(np.uint32), 0))
+    assert np.array_equal(np.where(valid, gi, 0), np.where(valid, ref["idx"], 0))
+
+
+def check_conv(got, x, w, b, shp, relu=False, images=None):
+    images = range(x.shape[0]) if images is None else images
+    worst = 0.0
+    for i0 in images:
+        ref, mass = oracle.conv_fp64(x[i0:i0 + 1], w, b, shp.stride, shp.pad, shp.groups)
+        if relu:
+            ref = np.maximum(ref, 0.0)
+        g = got[i0:i0 + 1].astype(np.float64)
+        err = np.abs(g - ref)
+        tol = oracle.tolerance_sparse(mass)
+        bad = err > tol
+        assert not bad.any(), (f"image {i0}: {bad.sum()} outputs out of tolerance; "
+                               f"max err {err.max():.3e} max ratio {(err / tol).max():.3f}")
+        worst = max(worst, float((err / tol).max()))
+    return worst
+
+
+SPARSE_CASES = [("C1", 0.9), ("C2", 0.9), ("C2", 0.95), ("C2", 0.99), ("C3", "channel"), ("C4a", 0.9),
+                ("C4a", 0.95), ("C4a", 0.99), ("C4b", 0.9), ("C4b", 0.95), ("C4b", 0.99)]
+
+
+@pytest.mark.parametrize("cfg,s", SPARSE_CASES)
+def test_full_config_lists_bitexact_and_sampled_outputs(sc, cfg, s):
+    """BASELINE sizes in the bench's launch configuration: whole batch through
+    sparse_conv_forward; lists bit-exact for the whole batch, outputs checked
+    on images {0, 1, middle, last}."""
+    shp = datagen.CONFIGS[cfg]
+    x = datagen.activations(shp, s)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b)
+    xd = torch.from_numpy(x).to(DEV)
+    out = conv.forward(xd)
+    torch.cuda.synchronize()
+    check_lists(conv, x, shp.n)
+    got = out.cpu().numpy()
+    check_conv(got, x, w, b, shp, images=[0, 1, shp.n // 2, shp.n - 1])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4a", "C4b"])
+@pytest.mark.parametrize("s", [0.0, 0.5, 0.95])
+def test_small_batch_all_outputs(sc, cfg, s):
+    """Every output of a 3-image batch (spans all tiles and ragged tails),
+    including dense (s=0) input: the sparse path must still meet 1e-5."""
+    shp = datagen.CONFIGS[cfg].with_batch(3)
+    x = datagen.activations(shp, s if cfg != "C3" or s == 0.0 else "channel", seed=5)
+    w, b = datagen.weights(shp, seed=5)
+    conv = make_conv(sc, shp, w, b, max_batch=8)
+    out = conv.forward(torch.from_numpy(x).to(DEV))
+    torch.cuda.synchronize()
+    check_lists(conv, x, 3)
+    check_conv(out.cpu().numpy(), x, w, b, shp)
+
+
+def test_table2_shapes(sc):
+    """Paper Table 2 shapes incl. stride 2 and 1x1, at their
+    printed sparsity, N=2, all outputs."""
+    for shp, s in datagen.table2_shapes(n=2):
+        x = datagen.activations(shp, s)
+        w, b = datagen.weights(shp)
+        conv = make_conv(sc, shp, w, b)
+        out = conv.forward(torch.from_numpy(x).to(DEV))
+        torch.cuda.synchronize()
+        check_lists(conv, x, 2)
+        check_conv(out.cpu().numpy(), x, w, b, shp)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4a", "C4b"])
+def test_integer_data_bitexact(sc, cfg):
+    shp = datagen.CONFIGS[cfg].with_batch(4)
+    x, w, b = datagen.integer_case(shp, sparsity=0.6)
+    conv = make_conv(sc, shp, w, b)
+    out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    ref, _ = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
+    assert np.array_equal(out.astype(np.float64), ref)
+
+
+def test_integer_data_bitexact_table2(sc):
+    for shp, _ in datagen.table2_shapes(n=2):
+        x, w, b = datagen.integer_case(shp, sparsity=0.7)
+        conv = make_conv(sc, shp, w, b)
+        out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+        ref, _ = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
+        assert np.array_equal(out.astype(np.float64), ref), shp.name
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4b"])
+def test_zero_input_gives_bias(sc, cfg):
+    shp = datagen.CONFIGS[cfg].with_batch(2)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b)
+    x = torch.zeros((2, shp.c, shp.h, shp.w), device=DEV)
+    out = conv.forward(x).cpu().numpy()
+    assert np.array_equal(out, np.broadcast_to(b[None, :, None, None], out.shape))
+    lists = conv.lists(2)
+    assert int(lists["counts"].sum()) == 0
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4a"])
+def test_one_hot_flipped_footprint(sc, cfg):
+    """Single nonzero v at (c,i,j), bias 0: out = fl32(v*W[k,c,i+P-y,j+P-x]),
+    bit-exact (one rounded product per output)."""
+    shp = datagen.CONFIGS[cfg].with_batch(1)
+    w, _ = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, None)
+    for (ci, i, j) in [(0, 0, 0), (shp.c - 1, shp.h - 1, shp.w - 1), (shp.c // 2, shp.h // 2, 1)]:
+        x = np.zeros((1, shp.c, shp.h, shp.w), np.float32)
+        v = np.float32(1.3125)
+        x[0, ci, i, j] = v
+        out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+        g = ci // (shp.c // shp.groups)
+        kg = shp.k // shp.groups
+        exp = np.zeros_like(out)
+        for y in range(shp.ho):
+            for xo in range(shp.wo):
+                r, t = i + shp.pad - y, j + shp.pad - xo
+                if 0 <= r < shp.r and 0 <= t < shp.s:
+                    exp[0, g * kg:(g + 1) * kg, y, xo] = v * w[g * kg:(g + 1) * kg, ci % (shp.c // shp.groups), r, t]
+        assert np.array_equal(out, exp)
+
+
+def test_subnormal_inputs_count_as_nonzero(sc):
+    """R7: subnormal inputs are nonzero (no FTZ anywhere)."""
+    shp = datagen.C2.with_batch(1)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, None)
+    x = np.zeros((1, shp.c, shp.h, shp.w), np.float32)
+    x[0, 3, 5, 6] = np.float32(1e-40)
+    x[0, 7, 0, 0] = np.float32(-0.0)
+    conv.compact(torch.from_numpy(x).to(DEV))
+    torch.cuda.synchronize()
+    check_lists(conv, x, 1)
+    assert int(conv.lists(1)["counts"].sum()) == 1
+    ws = np.full_like(w, 2.0 ** 100)
+    conv2 = make_conv(sc, shp, ws, None)
+    out = conv2.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    assert out[0, 0, 5, 6] == np.float32(np.float64(np.float32(1e-40)) * 2.0 ** 100)
+
+
+def test_ragged_batch_and_determinism(sc):
+    shp = datagen.C2.with_batch(5)
+    x = datagen.activations(shp, 0.95)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b, max_batch=16)
+    xd = torch.from_numpy(x).to(DEV)
+    o1 = conv.forward(xd).cpu().numpy()
+    o2 = conv.forward(xd).cpu().numpy()
+    assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
+    o3 = conv.forward(xd[:2].contiguous()).cpu().numpy()
+    assert np.array_equal(o3.view(np.uint32), o1[:2].view(np.uint32))
+    check_conv(o1, x, w, b, shp)
+
+
+def test_fused_relu_flag(sc):
+    shp = datagen.C2.with_batch(2)
+    x = datagen.activations(shp, 0.9)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b, relu=True)
+    out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    assert out.min() >= 0.0
+    check_conv(out, x, w, b, shp, relu=True)
+
+
+def test_forward_host_matches_device(sc):
+    shp = datagen.C4B.with_batch(6)
+    x = datagen.activations(shp, 0.95)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b)
+    dev = conv.forward(torch.from_numpy(x).to(DEV)).cpu()
+    h_in = torch.from_numpy(x).pin_memory()
+    h_out = torch.empty((6,) + conv.out_shape).pin_memory()
+    conv.forward_host(h_in, h_out)
+    assert torch.equal(dev, h_out)
+
+
+def test_argument_errors(sc):
+    shp = datagen.C4B.with_batch(2)
+    w, b = datagen.weights(shp)
+    conv = make_conv(sc, shp, w, b)
+    x = torch.zeros((3, shp.c, shp.h, shp.w), device=DEV)
+    with pytest.raises(sc.SparseConvError) as e:      # n > max batch
+        conv.forward(x)
+    assert e.value.status == 1
+    L = sc.lib()
+    import ctypes
+    out = torch.zeros((2,) + conv.out_shape, device=DEV)
+    xs = torch.zeros(2 * shp.c * shp.h * shp.w + 1, device=DEV)
+    st = L.sparse_conv_forward(conv._plan, 2, ctypes.c_void_p(xs.data_ptr() + 4), ctypes.c_void_p(out.data_ptr()), None)
+    assert st == 1 and b"aligned" in L.sc_last_error()
+    hx = torch.zeros(2 * shp.c * shp.h * shp.w)
+    st = L.sparse_conv_forward(conv._plan, 2, ctypes.c_void_p(hx.data_ptr()), ctypes.c_void_p(out.data_ptr()), None)
+    assert st == 1
+    assert L.sparse_conv_forward(conv._plan, 0, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(out.data_ptr()), None) == 1
+
+
+def test_c5_chain_per_layer(sc):
+    """C5 chain (R13/R14): each layer's oracle is fed the GPU's own input to
+    that layer; lists bit-exact on that tensor; ReLU'd outputs compared with
+    max(0, oracle).  Reduced batch (the full N=1024 chain is the bench's)."""
+    n = 8
+    layers = datagen.c5_weights()
+    x = datagen.activations(datagen.C5_LAYERS[0].with_batch(n), datagen.C5_FIRST_SPARSITY)
+    xd = torch.from_numpy(x).to(DEV)
+    for li, (shp, (w, b)) in enumerate(zip(datagen.C5_LAYERS, layers)):
+        shp = shp.with_batch(n)
+        relu = li < 2
+        conv = make_conv(sc, shp, w, b, relu=relu)
+        out = conv.forward(xd)
+        torch.cuda.synchronize()
+        xin = xd.cpu().numpy()
+        check_lists(conv, xin, n)
+        check_conv(out.cpu().numpy(), xin, w, b, shp, relu=relu)
+        if relu:
+            s = 1.0 - float((out != 0).sum()) / out.numel()
+            assert 0.9 < s < 0.99, s
+        xd = out
