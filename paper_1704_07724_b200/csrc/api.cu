@@ -18,7 +18,7 @@ struct sc_plan_s {
     int device;
     Geometry g;
     DenseGeom dg;
-    float* wpack = nullptr;    // [G][Cg][R][S][Kg_pad]
+    float* wpack = nullptr;    // [G][Kg_pad/32][Cg][R][S][32] (pack.cu)
     float* wdense = nullptr;   // [G][m_pad][kdim_pad], TF32-rounded (dense path)
     float* bias = nullptr;     // [K]
     float* values = nullptr;   // [num_lists][cap]

@@ -1,17 +1,44 @@
-// Shape-specialised stage-2 kernels (filled in below).
+// Stage 2 dispatch: pick the shape-specialised register-tile kernel
+// (gather_fast_impl.cuh; one translation unit per variant, gather_fast_vN.cu).
 #include "sc_internal.h"
 
 namespace sc {
+namespace fast {
+#include "gather_variants.inc"
+template <class V>
+bool matches(const Geometry& g) {
+    return g.T == 1 && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1;
+}
+#define SC_DECLARE(VV)                                                                                   \
+    cudaError_t launch_##VV(const Geometry& g, int64_t n, const float* values, const void* idx,          \
+                            const uint32_t* counts, const float* wpack, const float* bias, float* out,   \
+                            cudaStream_t st);
+SC_GATHER_VARIANTS(SC_DECLARE)
+#undef SC_DECLARE
+}  // namespace fast
 
 int gather_fast_select(const Geometry& g, const char** name) {
-    (void)g;
-    (void)name;
+    using namespace fast;
+    if (g.idx_bytes != 1) return 0;
+#define SC_SELECT(VV)            \
+    if (matches<VV>(g)) {        \
+        if (name) *name = VV::NAME; \
+        return VV::ID;           \
+    }
+    SC_GATHER_VARIANTS(SC_SELECT)
+#undef SC_SELECT
     return 0;
 }
 
-cudaError_t launch_gather_fast(int, const Geometry&, int64_t, const float*, const void*, const uint32_t*,
-                               const float*, const float*, float*, cudaStream_t) {
-    return cudaErrorNotSupported;
+cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const float* values, const void* idx,
+                               const uint32_t* counts, const float* wpack, const float* bias, float* out,
+                               cudaStream_t st) {
+    using namespace fast;
+#define SC_LAUNCH(VV) \
+    if (variant == VV::ID) return launch_##VV(g, n, values, idx, counts, wpack, bias, out, st);
+    SC_GATHER_VARIANTS(SC_LAUNCH)
+#undef SC_LAUNCH
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace sc

@@ -5,7 +5,7 @@
 //
 // out[n,k,y,x] = bias[k] + sum over nonzero inputs (c,i,j) of the lists whose
 // receptive-field tap (r,t) = (i + P - y*T, j + P - x*T) is inside R x S of
-//   v * wpack[g][cl][r][t][k]
+//   v * wpack[g][kb][cl][r][t][lane]   (k = 32*kb + lane, pack.cu)
 // i.e. exactly Eq. 1 with the zero terms skipped.
 //
 // Mapping: one warp per (n, group, 32-channel block, output row y, 32-column
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
         const int64_t tile_lo = i_first / th, tile_hi = i_last / th;
         for (int64_t cl = 0; cl < Cg; ++cl) {
             const int64_t c = g * Cg + cl;
-            const float* wc = wpack + (g * Cg + cl) * R * S * Kg_pad + kb * 32 + lane;
+            const float* wc = wpack + ((g * kblocks + kb) * Cg + cl) * R * S * 32 + lane;
             for (int64_t tile = tile_lo; tile <= tile_hi; ++tile) {
                 const int64_t list = (n * C + c) * tiles + tile;
                 const uint32_t cnt = counts[list];
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
                         if (num % T) continue;
                         const int64_t xo = num / T;
                         if (xo < x0 || xo >= x0 + 32 || xo >= Wo) continue;
-                        acc[xo - x0][lane] = fmaf(v, wc[(r * S + t) * Kg_pad], acc[xo - x0][lane]);
+                        acc[xo - x0][lane] = fmaf(v, wc[(r * S + t) * 32], acc[xo - x0][lane]);
                     }
                 }
             }

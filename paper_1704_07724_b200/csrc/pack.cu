@@ -5,10 +5,14 @@
 // that stores kernels (say 4 floats of weights: W_{k..k+3,c,i-r,j-s}) can be
 // fetched".  On the GPU the contiguous run over k is a warp's 32 lanes:
 //
-//   wpack[g][cl][r][t][kk] = W[g*Kg + kk][cl][r][t]   (kk < Kg; zero for kk in [Kg, Kg_pad))
+//   wpack[g][kb][cl][r][t][lane] = W[g*Kg + 32*kb + lane][cl][r][t]
+//   (zero for 32*kb + lane >= Kg; kb < Kg_pad/32)
 //
-// so lane kk of a warp reads consecutive 4-byte words (conflict-free shared
-// memory, coalesced global memory).
+// so lane k of a warp reads consecutive 4-byte words (conflict-free shared
+// memory, coalesced global memory), and the slice of CH consecutive input
+// channels for one 32-channel block kb is ONE contiguous run of
+// CH*R*S*128 bytes -- a single 1-D TMA bulk copy (cp.async.bulk) in the
+// gather kernel.
 #include "sc_internal.h"
 
 namespace sc {
@@ -18,12 +22,16 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
     const int64_t total = G * Cg * RS * Kg_pad;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
          o += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t kk = o % Kg_pad;
-        const int64_t rest = o / Kg_pad;          // ((g*Cg + cl)*RS + rs)
+        const int64_t lane = o % 32;
+        int64_t rest = o / 32;                    // ((g*kblocks + kb)*Cg + cl)*RS + rs
         const int64_t rs = rest % RS;
-        const int64_t gcl = rest / RS;
-        const int64_t cl = gcl % Cg;
-        const int64_t g = gcl / Cg;
+        rest /= RS;
+        const int64_t cl = rest % Cg;
+        rest /= Cg;
+        const int64_t kblocks = Kg_pad / 32;
+        const int64_t kb = rest % kblocks;
+        const int64_t g = rest / kblocks;
+        const int64_t kk = kb * 32 + lane;
         float v = 0.0f;
         if (kk < Kg) v = w[((g * Kg + kk) * Cg + cl) * RS + rs];
         wpack[o] = v;

@@ -6,7 +6,7 @@
 // probes measure what one SM actually retires per SM clock for
 //   kind 0: FFMA  Rd, Ra, Rb, Rc                (1 FMA per lane)
 //   kind 1: FFMA2 Rd, Ra.F32x2, Rb.F32, Rc.F32x2 (2 FMAs per lane, scalar bcast)
-//   kind 2: kind 1 with one independent integer op issued per FFMA2
+//   kind 2: kind 1 with ~2 independent ALU-pipe integer ops per FFMA2
 // using clock64() around an unrolled loop of independent accumulator chains
 // (one CTA of 1024 threads per SM, so every SMSP has 8 warps).
 #include "sc_internal.h"
@@ -47,17 +47,16 @@ __global__ void __launch_bounds__(1024, 1) probe_ffma2_kernel(const float* __res
     float2 acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = make_float2(src[1] + threadIdx.x, src[1] - i);
-    unsigned ia = threadIdx.x, ib = blockIdx.x;
+    unsigned ic[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ic[i] = threadIdx.x + 77u * i;
     __syncthreads();
     const long long t0 = clock64();
     for (int it = 0; it < kProbeIters; ++it) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             acc[i] = __ffma2_rn(w[i & 3], vv, acc[i]);
-            if (kWithInt) {
-                ia = ia + ib + (unsigned)i;
-                ib = ib ^ ia;
-            }
+            if (kWithInt) ic[i & 7] = (ic[i & 7] ^ (ic[i & 7] >> 3)) + 0x9e37u;  // 8 independent ALU chains
         }
     }
     __syncthreads();
@@ -65,7 +64,12 @@ __global__ void __launch_bounds__(1024, 1) probe_ffma2_kernel(const float* __res
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) s += acc[i].x + acc[i].y;
-    if (kWithInt) s += (float)(ia & 1u) + (float)(ib & 1u);
+    if (kWithInt) {
+        unsigned u = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u ^= ic[i];
+        s += (float)(u & 1u);
+    }
     dst[blockIdx.x * blockDim.x + threadIdx.x] = s;
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
