@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -18,7 +19,7 @@ struct sc_plan_s {
     int device;
     Geometry g;
     DenseGeom dg;
-    float* wpack = nullptr;    // [G][Kg_pad/32][Cg][R][S][32] (pack.cu)
+    float* wpack = nullptr;    // [G][Kg_pad/kbw][Cg][R][S][kbw] (pack.cu)
     float* wdense = nullptr;   // [G][m_pad][kdim_pad], TF32-rounded (dense path)
     float* bias = nullptr;     // [K]
     float* values = nullptr;   // [num_lists][cap]
@@ -82,6 +83,7 @@ sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg) {
     g->Wo = (p->w + 2 * p->pad - p->s) / p->stride + 1;
     g->Cg = p->c / p->groups;
     g->Kg = p->k / p->groups;
+    g->kbw = 32;  // set to 32*KL once the stage-2 variant is chosen (finish_geometry)
     g->Kg_pad = (g->Kg + 31) / 32 * 32;
     g->kblocks = g->Kg_pad / 32;
     g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
@@ -97,6 +99,19 @@ sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg) {
     if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || l_e > kMaxElems || d_e > kMaxElems)
         return fail(SC_ERR_UNSUPPORTED, "a tensor has >= 2^31 elements");
     return SC_OK;
+}
+
+// Choose the stage-2 kernel (SC_FORCE_VARIANT env: -1 auto, 0 generic, id) and
+// fix the packed-weight k-block width it needs.
+void finish_geometry(Geometry* g, int* variant, const char** name) {
+    int force = -1;
+    if (const char* f = getenv("SC_FORCE_VARIANT")) force = atoi(f);
+    int kl = 1;
+    *variant = sc::gather_fast_select(*g, force, name, &kl);
+    if (*variant == 0) *name = "generic";
+    g->kbw = 32 * kl;
+    g->Kg_pad = (g->Kg + g->kbw - 1) / g->kbw * g->kbw;
+    g->kblocks = g->Kg_pad / g->kbw;
 }
 
 sc_status check_dev_ptr(const sc_plan_s* plan, const void* ptr, const char* name) {
@@ -202,11 +217,12 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         delete plan;
         return st;
     }
+    finish_geometry(&plan->g, &plan->variant, &plan->variant_name);
     const Geometry& g = plan->g;
     const DenseGeom& dg = plan->dg;
     cudaError_t e;
     const size_t wbytes = sizeof(float) * g.G * g.Cg * g.R * g.S * g.Kg_pad;
-    const size_t dbytes = sizeof(float) * g.G * dg.m_pad * dg.kdim_pad;
+    const size_t dbytes = sizeof(float) * (g.G * dg.m_pad * dg.kdim_pad + 2 * dg.kdim_pad);
     if ((e = cudaMalloc(&plan->wpack, wbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->wdense, dbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
@@ -221,6 +237,10 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         e = cudaMemcpyAsync(plan->bias, d_bias, sizeof(float) * g.K, cudaMemcpyDeviceToDevice, st0);
     else
         e = cudaMemsetAsync(plan->bias, 0, sizeof(float) * g.K, st0);
+    // list slack is never interpreted (masked by counts) but is read by the
+    // register-tile kernel's 32-entry prefetch: keep it initialised
+    if (e == cudaSuccess) e = cudaMemsetAsync(plan->values, 0, sizeof(float) * g.num_lists * g.cap, st0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(plan->idx, 0, (size_t)g.idx_bytes * g.num_lists * g.cap, st0);
     if (e == cudaSuccess) e = sc::launch_pack_weights(g, d_weight, plan->wpack, st0);
     if (e == cudaSuccess) e = sc::launch_pack_dense(g, dg, d_weight, plan->wdense, st0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st0);
@@ -228,9 +248,6 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         free_plan(plan);
         return cuda_fail(e, "sparse_conv_create: pack");
     }
-    const char* name = nullptr;
-    plan->variant = sc::gather_fast_select(g, &name);
-    plan->variant_name = plan->variant ? name : "generic";
     *out_plan = plan;
     return SC_OK;
 }

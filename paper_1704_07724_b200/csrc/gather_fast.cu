@@ -17,13 +17,17 @@ SC_GATHER_VARIANTS(SC_DECLARE)
 #undef SC_DECLARE
 }  // namespace fast
 
-int gather_fast_select(const Geometry& g, const char** name) {
+// force < 0: first matching variant; force == 0: generic; force > 0: that
+// variant if it matches the geometry (else generic).
+int gather_fast_select(const Geometry& g, int force, const char** name, int* kl) {
     using namespace fast;
-    if (g.idx_bytes != 1) return 0;
-#define SC_SELECT(VV)            \
-    if (matches<VV>(g)) {        \
-        if (name) *name = VV::NAME; \
-        return VV::ID;           \
+    *kl = 1;
+    if (g.idx_bytes != 1 || force == 0) return 0;
+#define SC_SELECT(VV)                                   \
+    if (matches<VV>(g) && (force < 0 || force == VV::ID)) { \
+        if (name) *name = VV::NAME;                     \
+        *kl = VV::KL;                                   \
+        return VV::ID;                                  \
     }
     SC_GATHER_VARIANTS(SC_SELECT)
 #undef SC_SELECT

@@ -1,32 +1,31 @@
 // Stage 2, shape-specialised: output-stationary sparse-gather convolution
-// with the output tile in registers.
+// with the output tile in registers (template; one .cu per variant).
 //
 // Computes, for stride 1 (ISC steps 2-3; Eq. 1 P:68-72 with the
 // zero terms skipped):
 //   out[n,k,y,x] = bias[k] + sum_{c in group, nonzero in[n,c,i,j]} in * W[k,c,i+P-y,j+P-x]
 //
 // Mapping:
-//  * CTA = 8 warps sharing one (group g, 32-output-channel block kb).  The
-//    packed weight slice wpack[g][kb][c0:c0+CH][R][S][32] of CH input channels
-//    is ONE contiguous run and is streamed through a STAGES-deep shared-memory
-//    ring by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx);
-//    warp 0 lane 0 refills a stage once all 8 warps released it (empty
-//    mbarrier, 8 arrivals).
-//  * warp = one unit (image n, output rows [y0, y0+TY)); lane = output channel
-//    k = 32*kb + lane ("4 floats of weights ... at one time", becomes
-//    32 lanes).  The warp's tile acc[TY][NP] (pairs of adjacent x) lives in
-//    registers for the whole reduction over input channels.
-//  * per input channel: the lane's R*S weights come from shared memory (one
-//    conflict-free LDS per tap) and are arranged as pairs (W[r][u], W[r][u-1]);
-//    the channel's nonzero lists (stage-1 output, warp-uniform) are staged 32
-//    entries at a time into a per-warp shared buffer, keeping only entries
-//    inside the tile's input window, then each entry is one indirect branch
-//    (switch -> BRX) into generated code that applies FFMA2 to exactly the
-//    accumulators the entry reaches (tools/gen_gather.py).
+//  * CTA = NW warps sharing one (group g, k-block kb of KBW = 32*KL output
+//    channels).  The packed weight slice wpack[g][kb][c0:c0+CH][R][S][KBW] of
+//    CH input channels is ONE contiguous run, streamed through a STAGES-deep
+//    shared-memory ring by 1-D TMA bulk copies (cp.async.bulk + mbarrier
+//    complete_tx); thread 0 refills a stage once all NW warps released it.
+//  * warp = one unit (image n, output rows [y0, y0+TY)); lane owns KL output
+//    channels (the paper's "4 floats of weights ... at one time", P:123,
+//    becomes 32*KL per warp).  The warp's tile acc[TY][NX] (f32x2 pairs) stays
+//    in registers for the whole reduction over input channels.
+//  * per input channel: the lane's R*S weights come from the ring (conflict-
+//    free LDS), the channel's nonzero list (stage-1 output, warp-uniform) is
+//    staged 32 entries at a time into a per-warp shared buffer keeping only
+//    entries inside the tile's input window; each entry is one indirect,
+//    warp-uniform branch (brx.idx.uni) into generated code that applies
+//    FFMA2/FFMA to exactly the accumulators the entry reaches
+//    (tools/gen_gather.py).
 //  * epilogue (ISC step 3, "transpose temporary results"): registers ->
-//    per-warp shared buffer [k][x] -> contiguous NCHW row runs, + bias, optional
-//    ReLU (Eq. 2).  One global write per output, no atomics; accumulation order
-//    (channel, entry) is fixed, so results are deterministic.
+//    per-warp shared buffer [k][pixels] -> contiguous NCHW runs, + bias,
+//    optional ReLU (Eq. 2).  One global write per output, no atomics;
+//    accumulation order (channel, entry) is fixed -> deterministic.
 #pragma once
 #include "sc_internal.h"
 
@@ -35,8 +34,16 @@ namespace fast {
 
 #include "gather_variants.inc"
 
-constexpr int NW = 8;          // warps per CTA
-constexpr int kLookahead = 2;  // list segments whose first 32 entries are prefetched
+constexpr int kSegRing = 32;  // list segments in flight per warp (cp.async ring, ~2 chunks)
+constexpr int kEntCap = 256;  // entries of the per-warp stream buffer
+
+// One prefetched list segment: count + first 32 values + first 32 u8 indices.
+struct __align__(16) SegSlot {
+    float v[32];
+    uint32_t i4[8];
+    uint32_t cnt;
+    uint32_t pad[3];
+};
 
 struct Args {
     const float* values;
@@ -70,6 +77,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -79,27 +94,34 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 
 template <class V>
 struct Smem {
-    static constexpr int kStageFloats = V::CH * V::R * V::S * 32;
-    static constexpr int kER = (96 / V::WO) > 0 ? (96 / V::WO < V::TY ? 96 / V::WO : V::TY) : 1;  // epilogue rows
-    static constexpr int kEpiStride = (kER * V::WO) | 1;                                        // odd: no conflicts
+    static constexpr int KBW = 32 * V::KL;
+    static constexpr int kStageFloats = V::CH * V::R * V::S * KBW;
+    // epilogue rows per pass: KBW x (kER*WO) floats per warp ~ 8 KB
+    static constexpr int kERraw = (2048 / KBW) / V::WO;
+    static constexpr int kER = kERraw < 1 ? 1 : (kERraw > V::TY ? V::TY : kERraw);
+    static constexpr int kEpiStride = (kER * V::WO) | 1;                                        // odd
     static constexpr size_t ring = sizeof(float) * V::STAGES * kStageFloats;
     static constexpr size_t bars = 16 * V::STAGES;
-    static constexpr size_t ent = sizeof(uint2) * NW * 32;
-    static constexpr size_t epi = sizeof(float) * NW * 32 * kEpiStride;
-    static constexpr size_t total = ring + bars + ent + epi;
+    static constexpr size_t ent = sizeof(uint2) * V::NW * kEntCap;
+    static constexpr size_t seg = sizeof(SegSlot) * V::NW * kSegRing;
+    static constexpr size_t epi = sizeof(float) * V::NW * KBW * kEpiStride;
+    static constexpr size_t total = ring + bars + ent + seg + epi;
+    static_assert(total <= 227 * 1024, "shared memory budget of one CTA exceeded");
 };
 
 template <class V, typename IdxT>
-__global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
+__global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a) {
     using SM = Smem<V>;
-    constexpr int R = V::R, S = V::S, RS = R * S, TY = V::TY, NP = V::NP, WO = V::WO, W = V::W;
-    constexpr int CH = V::CH, STAGES = V::STAGES;
+    constexpr int R = V::R, RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO, W = V::W;
+    constexpr int CH = V::CH, STAGES = V::STAGES, NW = V::NW, KBW = SM::KBW;
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring);
     uint64_t* empty = full + STAGES;
     uint2* ent_all = reinterpret_cast<uint2*>(smem + SM::ring + SM::bars);
-    float* epi_all = reinterpret_cast<float*>(smem + SM::ring + SM::bars + SM::ent);
+    SegSlot* seg_all = reinterpret_cast<SegSlot*>(smem + SM::ring + SM::bars + SM::ent);
+    float* epi_all = reinterpret_cast<float*>(smem + SM::ring + SM::bars + SM::ent + SM::seg);
+    static_assert(sizeof(IdxT) == 1, "register-tile kernels read u8 list indices");
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cb = blockIdx.x % a.ctas_per_kb;
@@ -110,12 +132,15 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
     const int n = active ? unit / a.ytiles : 0;
     const int y0 = active ? (unit % a.ytiles) * TY : 0;
     const int nchunks = (a.Cg + CH - 1) / CH;
-    const float* wsrc = a.wpack + (size_t)gkb * a.Cg * RS * 32;
+    const float* wsrc = a.wpack + (size_t)gkb * a.Cg * RS * KBW;
 
+    // Warps without a unit (last CTA of a k-block) leave right after the
+    // barrier set-up; `empty` counts only the active warps of this CTA.
+    const int nactive = (a.units - cb * NW) < NW ? (a.units - cb * NW) : NW;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
+            mbar_init(&empty[s], (unsigned)nactive);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -123,11 +148,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
     if (threadIdx.x == 0) {
         for (int q = 0; q < STAGES && q < nchunks; ++q) {
             const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
-            const unsigned bytes = (unsigned)(chs * RS * 32 * sizeof(float));
+            const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
             mbar_expect_tx(&full[q], bytes);
-            tma_bulk_g2s(ring + q * SM::kStageFloats, wsrc + (size_t)q * CH * RS * 32, bytes, &full[q]);
+            tma_bulk_g2s(ring + q * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[q]);
         }
     }
+    if (!active) return;  // warp 0 is always active (every CTA has >= 1 unit)
 
     // Lists overlapping the input window rows [y0 - P, y0 + TY - 1 + R - 1 - P].
     int i_lo = y0 - V::P, i_hi = y0 + TY + R - 2 - V::P;
@@ -135,86 +161,77 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
     i_hi = i_hi > a.H - 1 ? a.H - 1 : i_hi;
     const int tl_lo = i_lo / a.th, nl = i_hi / a.th - tl_lo + 1;  // lists per channel (1..3)
 
-    // f32x2 accumulators as 64-bit patterns: x (= output column 2m) in the low word
-    unsigned long long acc[TY][NP];
+    unsigned long long acc[TY][NX];  // f32x2 bit patterns, low word = first element
 #pragma unroll
     for (int ty = 0; ty < TY; ++ty)
 #pragma unroll
-        for (int m = 0; m < NP; ++m) acc[ty][m] = 0ull;
+        for (int m = 0; m < NX; ++m) acc[ty][m] = 0ull;
 
-    uint2* ent = ent_all + warp * 32;
+    uint2* ent = ent_all + warp * kEntCap;
+    const unsigned ent_s = smem_u32(ent);
     const float* vbase = a.values;
     const IdxT* ibase = reinterpret_cast<const IdxT*>(a.idx);
+    // list id of channel cl, list l = (n*C + g*Cg + cl)*tiles + tl_lo + l
+    const int list0 = (n * a.C + g * a.Cg) * a.tiles + tl_lo;
 
-    // Segment = (channel cl, list tl_lo + l); global order s = cl * nl + l.
+    // Segment s = (channel s / nl, list s % nl).  A per-warp ring of kSegRing
+    // shared-memory slots receives, by cp.async (no registers held while in
+    // flight), the count and the first 32 entries of each segment, two weight
+    // chunks ahead of use.  The first 32 slots of a list are read regardless
+    // of its count (slack is zero-initialised at plan creation and masked).
     const int nseg = a.Cg * nl;
+    SegSlot* segring = seg_all + warp * kSegRing;
+    const int vlanes = a.cap < 32 ? a.cap : 32;
     auto seg_list = [&](int s) -> int {
-        const int cl = s / nl, l = s - cl * nl;
-        return (n * a.C + g * a.Cg + cl) * a.tiles + tl_lo + l;
+        const int cl = nl == 1 ? s : s / nl;
+        return list0 + cl * a.tiles + (s - cl * nl);
     };
-    // prefetch ring: counts and first 32 entries of segments s .. s+kLookahead
-    uint32_t pc[kLookahead + 1];
-    float pv[kLookahead + 1];
-    int pi[kLookahead + 1];
-    auto issue = [&](int s, int slot) {
+    auto issue = [&](int s) {
         if (active && s < nseg) {
-            const int list = seg_list(s);
-            const uint32_t cnt = __ldg(&a.counts[list]);
-            pc[slot] = cnt;
-            pv[slot] = (lane < (int)cnt) ? __ldg(&vbase[(size_t)list * a.cap + lane]) : 0.f;
-            pi[slot] = (lane < (int)cnt) ? (int)__ldg(&ibase[(size_t)list * a.cap + lane]) : 0;
-        } else {
-            pc[slot] = 0;
-            pv[slot] = 0.f;
-            pi[slot] = 0;
+            SegSlot* sl = segring + (s % kSegRing);
+            const size_t list = (size_t)seg_list(s);
+            if (lane < vlanes) cp_async4(&sl->v[lane], vbase + list * a.cap + lane);
+            if (lane < (vlanes + 3) / 4)
+                cp_async4(&sl->i4[lane], reinterpret_cast<const uint8_t*>(ibase) + list * a.cap + 4 * lane);
+            if (lane == 31) cp_async4(&sl->cnt, a.counts + list);
         }
+        cp_async_commit();
     };
-#pragma unroll
-    for (int d = 0; d <= kLookahead; ++d) issue(d, d);
+#pragma unroll 1
+    for (int d = 0; d < kSegRing; ++d) issue(d);
 
-    int s = 0;  // next segment to process
+    unsigned long long wp[V::NWOPS];
+#pragma unroll
+    for (int i = 0; i < V::NWOPS; ++i) wp[i] = 0ull;
+    int s = 0;  // next segment to stage
 #pragma unroll 1
     for (int ch = 0; ch < nchunks; ++ch) {
         const int st = ch % STAGES;
-        mbar_wait(&full[st], (ch / STAGES) & 1);
-        const float* wst = ring + st * SM::kStageFloats;
         const int cc_n = (a.Cg - ch * CH) < CH ? (a.Cg - ch * CH) : CH;
+        const unsigned wlane = smem_u32(ring + st * SM::kStageFloats) + lane * 4 * V::KL;
         if (active) {
+            // Stage this chunk's entry stream: per channel a LOADW entry, then
+            // its in-window nonzeros (ascending), finally EXIT.
+            int base = 0;
 #pragma unroll 1
             for (int cc = 0; cc < cc_n; ++cc) {
-                // wp[r][u] = (W[r][u], W[r][u-1]) with W[r][-1] = W[r][S] = 0
-                unsigned long long wp[R][S + 1];
-                {
-                    unsigned w[R][S];
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-#pragma unroll
-                        for (int t = 0; t < S; ++t) w[r][t] = __float_as_uint(wst[(cc * RS + r * S + t) * 32 + lane]);
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-#pragma unroll
-                        for (int u = 0; u <= S; ++u)
-                            wp[r][u] = (u < S ? (unsigned long long)w[r][u] : 0ull) |
-                                       ((u >= 1 ? (unsigned long long)w[r][u - 1] : 0ull) << 32);
-                }
+                if (lane == 0) ent[base] = make_uint2((unsigned)(cc * RS * KBW * 4), (unsigned)V::LOADW);
+                ++base;
 #pragma unroll 1
                 for (int l = 0; l < nl; ++l, ++s) {
-                    // rotate the prefetch ring: slot 0 is segment s
-                    const uint32_t cnt = pc[0];
-                    float v0 = pv[0];
-                    int i0 = pi[0];
-#pragma unroll
-                    for (int d = 0; d < kLookahead; ++d) {
-                        pc[d] = pc[d + 1];
-                        pv[d] = pv[d + 1];
-                        pi[d] = pi[d + 1];
-                    }
-                    issue(s + kLookahead + 1, kLookahead);
-                    const int list = seg_list(s);
+                    cp_async_wait<kSegRing - 1>();  // segment s has landed
+                    __syncwarp();
+                    SegSlot* sl = segring + (s % kSegRing);
+                    const uint32_t cnt = sl->cnt;
+                    float v0 = sl->v[lane];
+                    int i0 = (int)((sl->i4[lane >> 2] >> (8 * (lane & 3))) & 0xffu);
+                    __syncwarp();
+                    issue(s + kSegRing);  // refill this slot
                     const int off = ((tl_lo + l) * a.th - (y0 - V::P)) * W;
 #pragma unroll 1
                     for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
                         if (e0 > 0) {  // long list (dense input): synchronous loads
+                            const int list = seg_list(s);
                             const bool ok = e0 + lane < cnt;
                             v0 = ok ? vbase[(size_t)list * a.cap + e0 + lane] : 0.f;
                             i0 = ok ? (int)ibase[(size_t)list * a.cap + e0 + lane] : 0;
@@ -222,21 +239,24 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
                         const int cs = i0 + off;
                         const bool inwin = (e0 + lane < cnt) && cs >= 0 && cs < V::NCASES;
                         const unsigned bal = __ballot_sync(0xffffffffu, inwin);
-                        const int rank = __popc(bal & ((1u << lane) - 1u));
-                        if (inwin) ent[rank] = make_uint2(__float_as_uint(v0), (unsigned)cs);
-                        __syncwarp();
-                        const int nin = __popc(bal);
-                        uint2 nxt = ent[0];  // software-pipelined: next entry loads during this case
-#pragma unroll 1
-                        for (int e = 0; e < nin; ++e) {
-                            const uint2 t = nxt;
-                            nxt = ent[(e + 1) & 31];
-                            V::apply(acc, wp, __uint_as_float(t.x), (int)t.y);
+                        if (base + 32 + 2 > kEntCap) {  // stream full: run what we have
+                            if (lane == 0) ent[base] = make_uint2(0u, (unsigned)V::EXIT);
+                            __syncwarp();
+                            mbar_wait(&full[st], (ch / STAGES) & 1);
+                            V::run(acc, wp, ent_s, wlane);
+                            __syncwarp();
+                            base = 0;
                         }
-                        __syncwarp();
+                        const int rank = __popc(bal & ((1u << lane) - 1u));
+                        if (inwin) ent[base + rank] = make_uint2(__float_as_uint(v0), (unsigned)cs);
+                        base += __popc(bal);
                     }
                 }
             }
+            if (lane == 0) ent[base] = make_uint2(0u, (unsigned)V::EXIT);
+            __syncwarp();
+            mbar_wait(&full[st], (ch / STAGES) & 1);  // this chunk's weights have landed
+            V::run(acc, wp, ent_s, wlane);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -246,9 +266,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
                 const int qs = (ch - 1) % STAGES;
                 mbar_wait(&empty[qs], ((ch - 1) / STAGES) & 1);
                 const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
-                const unsigned bytes = (unsigned)(chs * RS * 32 * sizeof(float));
+                const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
                 mbar_expect_tx(&full[qs], bytes);
-                tma_bulk_g2s(ring + qs * SM::kStageFloats, wsrc + (size_t)q * CH * RS * 32, bytes, &full[qs]);
+                tma_bulk_g2s(ring + qs * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[qs]);
             }
         }
     }
@@ -256,18 +276,24 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
     if (!active) return;
     // Epilogue: registers -> smem [k][rows*WO] -> contiguous NCHW runs.
     constexpr int ER = SM::kER, ES = SM::kEpiStride;
-    float* epi = epi_all + warp * 32 * ES;
-    const int kloc = kb * 32;
+    float* epi = epi_all + warp * KBW * ES;
+    const int kloc = kb * KBW;
 #pragma unroll
     for (int r0 = 0; r0 < TY; r0 += ER) {
 #pragma unroll
         for (int rr = 0; rr < ER; ++rr) {
             if (r0 + rr < TY) {
 #pragma unroll
-                for (int m = 0; m < NP; ++m) {
-                    epi[lane * ES + rr * WO + 2 * m] = __uint_as_float((unsigned)acc[r0 + rr][m]);
-                    if (2 * m + 1 < WO)
-                        epi[lane * ES + rr * WO + 2 * m + 1] = __uint_as_float((unsigned)(acc[r0 + rr][m] >> 32));
+                for (int m = 0; m < NX; ++m) {
+                    const float lo = __uint_as_float((unsigned)acc[r0 + rr][m]);
+                    const float hi = __uint_as_float((unsigned)(acc[r0 + rr][m] >> 32));
+                    if constexpr (V::KL == 2) {  // (k = 2*lane, 2*lane+1) of pixel x = m
+                        epi[(2 * lane) * ES + rr * WO + m] = lo;
+                        epi[(2 * lane + 1) * ES + rr * WO + m] = hi;
+                    } else {                     // (x = 2m, 2m+1) of channel k = lane
+                        epi[lane * ES + rr * WO + 2 * m] = lo;
+                        if (2 * m + 1 < WO) epi[lane * ES + rr * WO + 2 * m + 1] = hi;
+                    }
                 }
             }
         }
@@ -276,7 +302,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gather_fast_kernel(const Args a) {
         if (y0 + r0 + rows > a.Ho) rows = a.Ho - (y0 + r0);
         if (rows > 0) {
             const int len = rows * WO;
-            for (int kk = 0; kk < 32; ++kk) {
+#pragma unroll 1
+            for (int kk = 0; kk < KBW; ++kk) {
                 const int k = kloc + kk;
                 if (k >= a.Kg) break;
                 const int kglob = g * a.Kg + k;
@@ -303,21 +330,20 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const float* values, const vo
     a.relu = g.relu ? 1 : 0;
     a.ytiles = (int)((g.Ho + V::TY - 1) / V::TY);
     a.units = (int)n * a.ytiles;
-    a.ctas_per_kb = (a.units + NW - 1) / NW;
+    a.ctas_per_kb = (a.units + V::NW - 1) / V::NW;
     const size_t smem = Smem<V>::total;
     auto kern = gather_fast_kernel<V, IdxT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(a);
+    kern<<<(unsigned)grid, V::NW * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 }  // namespace fast
 }  // namespace sc
 
-// Each gather_fast_vN.cu instantiates one variant (parallel compilation: ptxas
-// spends minutes on each jump-table kernel).
+// Each gather_fast_vN.cu instantiates one variant (parallel compilation).
 #define SC_INSTANTIATE_VARIANT(VV)                                                                         \
     namespace sc {                                                                                         \
     namespace fast {                                                                                       \

@@ -5,7 +5,7 @@
 //
 // out[n,k,y,x] = bias[k] + sum over nonzero inputs (c,i,j) of the lists whose
 // receptive-field tap (r,t) = (i + P - y*T, j + P - x*T) is inside R x S of
-//   v * wpack[g][kb][cl][r][t][lane]   (k = 32*kb + lane, pack.cu)
+//   v * wpack[g][kb][cl][r][t][j]   (k = kbw*kb + j, pack.cu)
 // i.e. exactly Eq. 1 with the zero terms skipped.
 //
 // Mapping: one warp per (n, group, 32-channel block, output row y, 32-column
@@ -23,16 +23,17 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
     const float* __restrict__ values, const IdxT* __restrict__ idx, const uint32_t* __restrict__ counts,
     const float* __restrict__ wpack, const float* __restrict__ bias, float* __restrict__ out,
     int64_t total_warps, int64_t C, int64_t H, int64_t W, int64_t K, int64_t R, int64_t S, int64_t T,
-    int64_t P, int64_t Cg, int64_t Kg, int64_t Kg_pad, int64_t Ho, int64_t Wo, int64_t th,
+    int64_t P, int64_t Cg, int64_t Kg, int64_t Kg_pad, int64_t kbw, int64_t Ho, int64_t Wo, int64_t th,
     int64_t tiles, int64_t cap, int relu) {
     __shared__ float acc_s[8][32][33];
     const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     int64_t wid = (int64_t)blockIdx.x * 8 + wib;
     if (wid >= total_warps) return;
-    const int64_t xblocks = (Wo + 31) / 32, kblocks = Kg_pad / 32, G = K / Kg;
+    const int64_t xblocks = (Wo + 31) / 32, kq32 = Kg_pad / 32, kblocks = Kg_pad / kbw, G = K / Kg;
     const int64_t xb = wid % xblocks; wid /= xblocks;
     const int64_t y = wid % Ho; wid /= Ho;
-    const int64_t kb = wid % kblocks; wid /= kblocks;
+    const int64_t kq = wid % kq32; wid /= kq32;   // 32-channel slice: k = 32*kq + lane
+    const int64_t kb = kq / (kbw / 32), khalf = kq % (kbw / 32);
     const int64_t g = wid % G;
     const int64_t n = wid / G;
     const int64_t x0 = xb * 32;
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
         const int64_t tile_lo = i_first / th, tile_hi = i_last / th;
         for (int64_t cl = 0; cl < Cg; ++cl) {
             const int64_t c = g * Cg + cl;
-            const float* wc = wpack + ((g * kblocks + kb) * Cg + cl) * R * S * 32 + lane;
+            const float* wc = wpack + ((g * kblocks + kb) * Cg + cl) * R * S * kbw + khalf * 32 + lane;
             for (int64_t tile = tile_lo; tile <= tile_hi; ++tile) {
                 const int64_t list = (n * C + c) * tiles + tile;
                 const uint32_t cnt = counts[list];
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
                         if (num % T) continue;
                         const int64_t xo = num / T;
                         if (xo < x0 || xo >= x0 + 32 || xo >= Wo) continue;
-                        acc[xo - x0][lane] = fmaf(v, wc[(r * S + t) * 32], acc[xo - x0][lane]);
+                        acc[xo - x0][lane] = fmaf(v, wc[(r * S + t) * kbw], acc[xo - x0][lane]);
                     }
                 }
             }
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
     __syncwarp();
     const int64_t x = x0 + lane;
     for (int kk = 0; kk < 32; ++kk) {
-        const int64_t k = kb * 32 + kk;
+        const int64_t k = kq * 32 + kk;
         if (k >= Kg) break;
         const int64_t kglob = g * Kg + k;
         if (x < Wo) {
@@ -91,16 +92,16 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
 cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const float* values, const void* idx,
                                   const uint32_t* counts, const float* wpack, const float* bias,
                                   float* out, cudaStream_t st) {
-    const int64_t total_warps = n * g.G * g.kblocks * g.Ho * ((g.Wo + 31) / 32);
+    const int64_t total_warps = n * g.G * (g.Kg_pad / 32) * g.Ho * ((g.Wo + 31) / 32);
     const int64_t blocks = (total_warps + 7) / 8;
     if (g.idx_bytes == 1)
         gather_generic_kernel<uint8_t><<<(unsigned)blocks, 256, 0, st>>>(
             values, (const uint8_t*)idx, counts, wpack, bias, out, total_warps, g.C, g.H, g.W, g.K, g.R,
-            g.S, g.T, g.P, g.Cg, g.Kg, g.Kg_pad, g.Ho, g.Wo, g.th, g.tiles, g.cap, g.relu ? 1 : 0);
+            g.S, g.T, g.P, g.Cg, g.Kg, g.Kg_pad, g.kbw, g.Ho, g.Wo, g.th, g.tiles, g.cap, g.relu ? 1 : 0);
     else
         gather_generic_kernel<uint16_t><<<(unsigned)blocks, 256, 0, st>>>(
             values, (const uint16_t*)idx, counts, wpack, bias, out, total_warps, g.C, g.H, g.W, g.K, g.R,
-            g.S, g.T, g.P, g.Cg, g.Kg, g.Kg_pad, g.Ho, g.Wo, g.th, g.tiles, g.cap, g.relu ? 1 : 0);
+            g.S, g.T, g.P, g.Cg, g.Kg, g.Kg_pad, g.kbw, g.Ho, g.Wo, g.th, g.tiles, g.cap, g.relu ? 1 : 0);
     return cudaGetLastError();
 }
 

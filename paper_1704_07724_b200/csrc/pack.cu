@@ -5,33 +5,33 @@
 // that stores kernels (say 4 floats of weights: W_{k..k+3,c,i-r,j-s}) can be
 // fetched".  On the GPU the contiguous run over k is a warp's 32 lanes:
 //
-//   wpack[g][kb][cl][r][t][lane] = W[g*Kg + 32*kb + lane][cl][r][t]
-//   (zero for 32*kb + lane >= Kg; kb < Kg_pad/32)
+//   wpack[g][kb][cl][r][t][j] = W[g*Kg + kbw*kb + j][cl][r][t]
+//   (zero for kbw*kb + j >= Kg; kb < Kg_pad/kbw; kbw = 32*KL of the stage-2 kernel)
 //
-// so lane k of a warp reads consecutive 4-byte words (conflict-free shared
-// memory, coalesced global memory), and the slice of CH consecutive input
-// channels for one 32-channel block kb is ONE contiguous run of
-// CH*R*S*128 bytes -- a single 1-D TMA bulk copy (cp.async.bulk) in the
+// so the lanes of a warp read consecutive 4-byte (KL=1) or 8-byte (KL=2)
+// words (conflict-free shared memory, coalesced global memory), and the slice
+// of CH consecutive input channels for one k-block is ONE contiguous run of
+// CH*R*S*kbw*4 bytes -- a single 1-D TMA bulk copy (cp.async.bulk) in the
 // gather kernel.
 #include "sc_internal.h"
 
 namespace sc {
 
 __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ wpack,
-                                    int64_t G, int64_t Kg, int64_t Kg_pad, int64_t Cg, int64_t RS) {
+                                    int64_t G, int64_t Kg, int64_t Kg_pad, int64_t Cg, int64_t RS, int64_t kbw) {
     const int64_t total = G * Cg * RS * Kg_pad;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
          o += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t lane = o % 32;
-        int64_t rest = o / 32;                    // ((g*kblocks + kb)*Cg + cl)*RS + rs
+        const int64_t j = o % kbw;
+        int64_t rest = o / kbw;                   // ((g*kblocks + kb)*Cg + cl)*RS + rs
         const int64_t rs = rest % RS;
         rest /= RS;
         const int64_t cl = rest % Cg;
         rest /= Cg;
-        const int64_t kblocks = Kg_pad / 32;
+        const int64_t kblocks = Kg_pad / kbw;
         const int64_t kb = rest % kblocks;
         const int64_t g = rest / kblocks;
-        const int64_t kk = kb * 32 + lane;
+        const int64_t kk = kb * kbw + j;
         float v = 0.0f;
         if (kk < Kg) v = w[((g * Kg + kk) * Cg + cl) * RS + rs];
         wpack[o] = v;
@@ -43,7 +43,7 @@ cudaError_t launch_pack_weights(const Geometry& g, const float* w, float* wpack,
     const int threads = 256;
     const int64_t blocks = (total + threads - 1) / threads;
     pack_weights_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, st>>>(
-        w, wpack, g.G, g.Kg, g.Kg_pad, g.Cg, g.R * g.S);
+        w, wpack, g.G, g.Kg, g.Kg_pad, g.Cg, g.R * g.S, g.kbw);
     return cudaGetLastError();
 }
 

@@ -13,8 +13,9 @@ namespace sc {
 struct Geometry {
     int64_t N, C, H, W, K, R, S, T, P, G;
     int64_t Ho, Wo, Cg, Kg;
-    int64_t Kg_pad;         // Kg rounded up to 32 (one warp of output channels)
-    int64_t kblocks;        // Kg_pad / 32
+    int64_t kbw;            // k-block width of the packed weights: 32 * KL of the stage-2 kernel
+    int64_t Kg_pad;         // Kg rounded up to kbw
+    int64_t kblocks;        // Kg_pad / kbw
     // stage-1 list format (reading R9)
     int64_t th, tiles, cap, idx_bytes, num_lists;  // num_lists for N images
     bool relu;
@@ -39,7 +40,7 @@ cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const float* val
 
 // Shape-specialised stage-2 kernels (gather_fast.cu).  `select` returns a
 // variant id > 0 if one applies to the geometry, else 0.
-int gather_fast_select(const Geometry& g, const char** name);
+int gather_fast_select(const Geometry& g, int force, const char** name, int* kl);
 cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const float* values,
                                const void* idx, const uint32_t* counts, const float* wpack,
                                const float* bias, float* out, cudaStream_t st);

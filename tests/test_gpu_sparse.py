@@ -261,3 +261,23 @@ def test_c5_chain_per_layer(sc):
             s = 1.0 - float((out != 0).sum()) / out.numel()
             assert 0.9 < s < 0.99, s
         xd = out
+
+
+@pytest.mark.parametrize("variant", [0, 1, 6])
+@pytest.mark.parametrize("s", [0.0, 0.95])
+def test_forced_variants_c2(sc, variant, s, monkeypatch):
+    """Every stage-2 kernel that matches C2 (generic=0, KL=2 tiles, KL=1 whole
+    plane) against the oracle, via SC_FORCE_VARIANT."""
+    monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
+    shp = datagen.C2.with_batch(5)
+    x = datagen.activations(shp, s, seed=3)
+    w, b = datagen.weights(shp, seed=3)
+    conv = make_conv(sc, shp, w, b, max_batch=9)
+    assert conv.variant[0] == variant
+    out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    check_conv(out, x, w, b, shp)
+    xi, wi, bi = datagen.integer_case(shp, sparsity=0.7)
+    conv = make_conv(sc, shp, wi, bi, max_batch=9)
+    out = conv.forward(torch.from_numpy(xi).to(DEV)).cpu().numpy()
+    ref, _ = oracle.conv_fp64(xi, wi, bi, 1, 1, 1)
+    assert np.array_equal(out.astype(np.float64), ref)
