@@ -70,21 +70,27 @@ typedef struct {
 typedef struct sc_plan_s *sc_plan;
 
 /* Read-only view of the stage-1 workspace (device pointers owned by the plan).
- * List format (reading R9): list id = (n*C + c)*tiles_per_plane + tile; a list
- * covers rows [tile*row_tile_h, min(H,(tile+1)*row_tile_h)) of plane (n,c);
- * entry e < counts[id] holds values[id*slot_capacity + e] (bit copy of an
- * input x with x != 0.0f) and idx[id*slot_capacity + e] = (row - tile*TH)*W +
- * col as u8 (idx_bytes 1) or u16 (idx_bytes 2), ascending.  Slots beyond the
- * count are undefined. */
+ * Tile-stream format (reading R9): output rows are cut into tiles
+ * of TY = tile_rows rows; tile t of image n has the input window of
+ * NWR = window_rows rows starting at input row t*TY*stride - pad, all W =
+ * window_width columns, NWIN = marker_code = NWR*W positions.  Its stream
+ * (stream id s = n*tiles_per_image + t) is entries[s*stream_capacity*2 ...],
+ * a sequence of u32 pairs (a, b):
+ *   for every input channel c ascending: the marker (a = c, b = NWIN), then
+ *   every input x = in[n,c,i,j] != 0.0f inside the window (ascending i, j)
+ *   as (a = bit copy of x, b = (i - (t*TY*stride - pad))*W + j).
+ * offsets[s*(C+1) + c] = index of channel c's marker, offsets[s*(C+1) + C] =
+ * stream length.  Entries beyond the length are undefined. */
 typedef struct {
-    const float *values;
-    const void *idx;
-    const uint32_t *counts;
-    int64_t num_lists;
-    int64_t slot_capacity;
-    int64_t tiles_per_plane;
-    int32_t row_tile_h;
-    int32_t idx_bytes;
+    const uint32_t *entries;   /* [N][tiles][stream_capacity][2] */
+    const uint32_t *offsets;   /* [N][tiles][channels + 1]       */
+    int64_t tiles_per_image;
+    int64_t stream_capacity;
+    int64_t channels;
+    int32_t tile_rows;
+    int32_t window_rows;
+    int32_t window_width;
+    int32_t marker_code;
 } sc_lists_view;
 
 /* Output shape (N = params.n): out_nchw = {n, k, H_out, W_out}.  Pure host

@@ -15,9 +15,9 @@ conv_fp64           P:68-72 (Eq. 1) + stride/pad + batch/bias/groups
                     (R2-R4); fp64 accumulation, also returns the mass
                     sum |in|*|W| that scales the parity tolerance.  (C, OpenMP)
 relu                P:74-78 (Eq. 2)
-list_format         R9: row-tile height TH, index width, slot capacity
-compact             P:123 (Sec. 4, ISC step 1) in the R9 list format  (C)
-decompress          inverse of compact (for round-trip pins)
+stream_format       R9: tiles, window rows, window size, stream capacity
+compact_streams     P:123 (Sec. 4, ISC step 1) in the R9 tile-stream format (C)
+decompress_streams  inverse of compact_streams (for round-trip pins)
 dense_macs          P:109 (Sec. 4): H_out*W_out*R*S*K*C per image (with groups:
                     C/G per output channel)
 exact_nonzero_macs  P:121 (Sec. 4) "MACs can be reduce to rho*...": the exact
@@ -62,8 +62,8 @@ def _load():
         vp = ctypes.c_void_p
         lib.oracle_conv_fp64.restype = ctypes.c_int
         lib.oracle_conv_fp64.argtypes = [vp, vp, vp] + [i64] * 10 + [vp, vp]
-        lib.oracle_compact.restype = ctypes.c_int
-        lib.oracle_compact.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp]
+        lib.oracle_compact_streams.restype = ctypes.c_int
+        lib.oracle_compact_streams.argtypes = [vp] + [i64] * 10 + [vp, vp]
         _lib = lib
     return _lib
 
@@ -161,53 +161,57 @@ def conv_fp64(x, w, bias=None, stride=1, pad=0, groups=1, want_mass=True):
 
 
 # --------------------------------------------------------------------------
-# ISC step 1: nonzero compaction in the R9 list format
+# ISC step 1: nonzero compaction in the R9 tile-stream format
 # --------------------------------------------------------------------------
-def list_format(h, w):
-    """DESIGN.md R9.  A list covers TH consecutive rows of one (n,c) plane:
-    TH = H when H*W <= 256, else floor(256/W) rows (>= 1).  idx is u8 when
-    TH*W <= 256 else u16.  Slot capacity = TH*W rounded up to 16 entries.
-    Returns (TH, tiles_per_plane, idx_bytes, cap)."""
-    if h * w <= 256:
-        th = h
-    else:
-        th = max(1, 256 // w)
-    idx_bytes = 1 if th * w <= 256 else 2
-    cap = -(-(th * w) // 16) * 16
-    tiles = -(-h // th)
-    return th, tiles, idx_bytes, cap
+def stream_format(c, h, w, r, stride, pad, ty, ho):
+    """DESIGN.md R9.  Row-tile t covers output rows [t*TY, (t+1)*TY); its input
+    window has NWR = (TY-1)*T + R rows starting at t*TY*T - P, all W columns;
+    NWIN = NWR*W.  Capacity of one (image, tile) stream = C markers + every
+    in-plane window position, rounded up to an even number of entries.
+    Returns (tiles, NWR, NWIN, cap)."""
+    tiles = -(-ho // ty)
+    nwr = (ty - 1) * stride + r
+    nwin = nwr * w
+    cap = c * (1 + min(nwr, h) * w)
+    cap += cap & 1
+    return tiles, nwr, nwin, cap
 
 
-def compact(x):
-    """P:123 step 1.  x float32 [N][C][H][W] -> dict(values [L][cap] f32,
-    idx [L][cap] u8/u16, counts [L] u32, th, tiles, idx_bytes, cap).
-    Slack beyond counts[l] is left zero-filled here and is never compared."""
+def compact_streams(x, r, stride, pad, ty):
+    """P:123 step 1.  x float32 [N][C][H][W] -> dict(entries u32 [N][tiles][cap][2],
+    offs u32 [N][tiles][C+1], tiles, nwr, nwin, cap).  Entries beyond
+    offs[..][C] are left zero here and are never compared."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n, c, h, w = x.shape
-    th, tiles, idx_bytes, cap = list_format(h, w)
-    nl = n * c * tiles
-    values = np.zeros((nl, cap), dtype=np.float32)
-    idx = np.zeros((nl, cap), dtype=np.uint8 if idx_bytes == 1 else np.uint16)
-    counts = np.zeros(nl, dtype=np.uint32)
-    rc = _load().oracle_compact(_ptr(x), n, c, h, w, th, idx_bytes, cap,
-                                _ptr(values), _ptr(idx), _ptr(counts))
+    ho = (h + 2 * pad - r) // stride + 1
+    tiles, nwr, nwin, cap = stream_format(c, h, w, r, stride, pad, ty, ho)
+    entries = np.zeros((n, tiles, cap, 2), dtype=np.uint32)
+    offs = np.zeros((n, tiles, c + 1), dtype=np.uint32)
+    rc = _load().oracle_compact_streams(_ptr(x), n, c, h, w, ty, tiles, r, stride, pad, cap,
+                                        _ptr(entries), _ptr(offs))
     if rc != 0:
-        raise ValueError("oracle_compact: invalid arguments")
-    return dict(values=values, idx=idx, counts=counts, th=th, tiles=tiles,
-                idx_bytes=idx_bytes, cap=cap)
+        raise ValueError("oracle_compact_streams: invalid arguments")
+    return dict(entries=entries, offs=offs, tiles=tiles, nwr=nwr, nwin=nwin, cap=cap, ty=ty)
 
 
-def decompress(lists, shape):
-    """Inverse of compact: scatter the entries back into a zero tensor."""
+def decompress_streams(st, shape, stride, pad):
+    """Inverse of compact_streams: scatter every stream's entries back into a
+    zero tensor (inputs in several windows are written more than once, with
+    the same bits).  Also checks the markers."""
     n, c, h, w = shape
-    th, tiles = lists["th"], lists["tiles"]
-    out = np.zeros((n * c, h * w), dtype=np.float32)
-    for l in range(n * c * tiles):
-        plane, tile = divmod(l, tiles)
-        cnt = int(lists["counts"][l])
-        loc = lists["idx"][l, :cnt].astype(np.int64) + tile * th * w
-        out[plane, loc] = lists["values"][l, :cnt]
-    return out.reshape(n, c, h, w)
+    out = np.zeros(shape, dtype=np.float32).reshape(n, c, h * w).view(np.uint32)
+    for ni in range(n):
+        for t in range(st["tiles"]):
+            i_lo = t * st["ty"] * stride - pad
+            e = st["entries"][ni, t]
+            of = st["offs"][ni, t]
+            for ci in range(c):
+                a, b = int(of[ci]), int(of[ci + 1])
+                assert e[a, 0] == ci and e[a, 1] == st["nwin"], "bad channel marker"
+                code = e[a + 1:b, 1].astype(np.int64)
+                rows = i_lo + code // w
+                out[ni, ci, rows * w + code % w] = e[a + 1:b, 0]
+    return out.view(np.float32).reshape(shape)
 
 
 def tolerance_sparse(mass):

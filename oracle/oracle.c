@@ -17,10 +17,10 @@
  *                        Accumulates in double, loop order n,k,y,x | c,r,t.
  *                        Also returns mass = sum |in|*|W| over the receptive
  *                        field (the tolerance scale of the north star).
- *   oracle_compact    -- ISC step 1, PAPER.md:123 (Sec. 4): "skip all the zero
- *                        elements of the input data, and store the non-zero
- *                        values in a vector with their column and row
- *                        information", in the list format of DESIGN.md R9.
+ *   oracle_compact_streams -- ISC step 1, PAPER.md:123 (Sec. 4): "skip all the
+ *                        zero elements of the input data, and store the
+ *                        non-zero values in a vector with their column and row
+ *                        information", in the tile-stream format of DESIGN.md R9.
  *
  * Build: gcc -O2 -fopenmp -fPIC -shared (no -ffast-math: rounding and IEEE
  * zero tests must be exact).
@@ -94,49 +94,61 @@ int oracle_conv_fp64(const float *in, const float *w, const float *bias,
 }
 
 /*
- * ISC step 1 in the list format of DESIGN.md R9.
+ * ISC step 1 in the tile-stream format of DESIGN.md R9:
+ * "store the non-zero values in a vector with their column and row
+ * information", one vector per (image n, output row-tile t).
  *
- * A list covers TH consecutive input rows of one (n, c) plane:
- *   list id  = (n*C + c) * tiles + tile,  tiles = ceil(H / TH)
- *   entries  = every element x of those rows with x != 0.0f (IEEE compare:
- *              -0.0 is zero, subnormals/NaN/Inf are nonzero), in ascending
- *              row-major scan order
- *   value    = bit copy of x
- *   idx      = (row - tile*TH) * W + col, stored as u8 (idx_bytes == 1) or
- *              u16 (idx_bytes == 2)
- *   count    = number of entries
- * values/idx are [num_lists][cap]; entries beyond count are not written.
- * Returns 0, or -1 on invalid arguments.
+ * Tile t covers output rows [t*TY, (t+1)*TY); its input window is rows
+ * i_lo = t*TY*T - P .. i_lo + NWR - 1 with NWR = (TY-1)*T + R, all W columns,
+ * NWIN = NWR*W window positions.  stream[n][t] is a sequence of 8-byte
+ * entries (a, b) (u32 pairs):
+ *   for c = 0..C-1 (ascending):
+ *     marker  (a = c, b = NWIN)
+ *     for every input x = in[n,c,i,j] != 0.0f (IEEE compare: -0.0 is zero;
+ *     subnormal/NaN/Inf are nonzero) with i inside the window and the plane,
+ *     ascending (i, j):  (a = bit copy of x, b = (i - i_lo)*W + j)
+ *   offs[n][t][c] = index of channel c's marker, offs[n][t][C] = length.
+ * entries: u32 [N][tiles][cap][2]; offs: u32 [N][tiles][C+1].  Entries beyond
+ * the length are not written.  Returns 0, or -1 on invalid arguments / overflow.
  */
-int oracle_compact(const float *in, int64_t N, int64_t C, int64_t H, int64_t W,
-                   int64_t TH, int64_t idx_bytes, int64_t cap,
-                   float *values, void *idx, uint32_t *counts)
+int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int64_t W,
+                           int64_t TY, int64_t tiles, int64_t R, int64_t T, int64_t P,
+                           int64_t cap, uint32_t *entries, uint32_t *offs)
 {
-    if (N < 1 || C < 1 || H < 1 || W < 1 || TH < 1 || TH > H) return -1;
-    if (idx_bytes != 1 && idx_bytes != 2) return -1;
-    if (TH * W > (idx_bytes == 1 ? 256 : 65536) || cap < TH * W) return -1;
-    const int64_t tiles = (H + TH - 1) / TH;
-    #pragma omp parallel for schedule(static)
-    for (int64_t plane = 0; plane < N * C; ++plane) {
-        for (int64_t tile = 0; tile < tiles; ++tile) {
-            const int64_t list = plane * tiles + tile;
-            uint32_t cnt = 0;
-            for (int64_t i = tile * TH; i < H && i < (tile + 1) * TH; ++i) {
-                for (int64_t j = 0; j < W; ++j) {
-                    const float x = in[(plane * H + i) * W + j];
-                    if (x != 0.0f) {
-                        const int64_t local = (i - tile * TH) * W + j;
-                        memcpy(&values[list * cap + cnt], &x, sizeof(float));
-                        if (idx_bytes == 1)
-                            ((uint8_t *)idx)[list * cap + cnt] = (uint8_t)local;
-                        else
-                            ((uint16_t *)idx)[list * cap + cnt] = (uint16_t)local;
-                        ++cnt;
+    if (N < 1 || C < 1 || H < 1 || W < 1 || TY < 1 || tiles < 1 || R < 1 || T < 1 || P < 0) return -1;
+    const int64_t NWR = (TY - 1) * T + R, NWIN = NWR * W;
+    int bad = 0;
+    #pragma omp parallel for collapse(2) schedule(static) reduction(|:bad)
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t t = 0; t < tiles; ++t) {
+            const int64_t i_lo = t * TY * T - P;
+            uint32_t *st = entries + (n * tiles + t) * cap * 2;
+            uint32_t *of = offs + (n * tiles + t) * (C + 1);
+            int64_t len = 0;
+            for (int64_t c = 0; c < C; ++c) {
+                of[c] = (uint32_t)len;
+                if (len >= cap) { bad = 1; break; }
+                st[2 * len] = (uint32_t)c;
+                st[2 * len + 1] = (uint32_t)NWIN;
+                ++len;
+                for (int64_t wi = 0; wi < NWR; ++wi) {
+                    const int64_t i = i_lo + wi;
+                    if (i < 0 || i >= H) continue;
+                    for (int64_t j = 0; j < W; ++j) {
+                        const float x = in[((n * C + c) * H + i) * W + j];
+                        if (x != 0.0f) {
+                            if (len >= cap) { bad = 1; break; }
+                            uint32_t bits;
+                            memcpy(&bits, &x, sizeof bits);
+                            st[2 * len] = bits;
+                            st[2 * len + 1] = (uint32_t)(wi * W + j);
+                            ++len;
+                        }
                     }
                 }
             }
-            counts[list] = cnt;
+            of[C] = (uint32_t)len;
         }
     }
-    return 0;
+    return bad ? -1 : 0;
 }

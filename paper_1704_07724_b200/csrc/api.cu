@@ -22,9 +22,8 @@ struct sc_plan_s {
     float* wpack = nullptr;    // [G][Kg_pad/kbw][Cg][R][S][kbw] (pack.cu)
     float* wdense = nullptr;   // [G][m_pad][kdim_pad], TF32-rounded (dense path)
     float* bias = nullptr;     // [K]
-    float* values = nullptr;   // [num_lists][cap]
-    void* idx = nullptr;       // [num_lists][cap] u8/u16
-    uint32_t* counts = nullptr;
+    uint2* entries = nullptr;  // stage-1 tile streams [N][tiles][cap] (+2 entries of slack)
+    uint32_t* offs = nullptr;  // [N][tiles][C+1]
     int variant = 0;
     const char* variant_name = "generic";
     // staging for sparse_conv_forward_host (allocated on first use)
@@ -68,50 +67,50 @@ sc_status validate_params(const sc_conv_params* p) {
     return SC_OK;
 }
 
-// Reading R9: list format.
-void list_format(int64_t H, int64_t W, int64_t* th, int64_t* tiles, int64_t* idx_bytes, int64_t* cap) {
-    *th = (H * W <= 256) ? H : ((256 / W) > 1 ? 256 / W : 1);
-    *idx_bytes = (*th * W <= 256) ? 1 : 2;
-    *cap = (*th * W + 15) / 16 * 16;
-    *tiles = (H + *th - 1) / *th;
+// Reading R9: tile-stream format for row tiles of `ty` output rows.
+void stream_format(Geometry* g, int64_t ty) {
+    g->ty = ty;
+    g->tiles = (g->Ho + ty - 1) / ty;
+    g->nwr = (ty - 1) * g->T + g->R;
+    g->nwin = g->nwr * g->W;
+    const int64_t rows = g->nwr < g->H ? g->nwr : g->H;
+    g->cap = g->C * (1 + rows * g->W);
+    g->cap += g->cap & 1;  // even: every stream starts 16-byte aligned
 }
 
-sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg) {
+// Choose the stage-2 kernel (SC_FORCE_VARIANT env: -1 auto, 0 generic, id) and
+// fix what it implies: packed-weight k-block width and the stream row tiles.
+void choose_kernel(Geometry* g, int* variant, const char** name) {
+    int force = -1;
+    if (const char* f = getenv("SC_FORCE_VARIANT")) force = atoi(f);
+    int kl = 1, ty = (int)g->Ho;
+    *variant = sc::gather_fast_select(*g, force, name, &kl, &ty);
+    if (*variant == 0) *name = "generic";
+    g->kbw = 32 * kl;
+    g->Kg_pad = (g->Kg + g->kbw - 1) / g->kbw * g->kbw;
+    g->kblocks = g->Kg_pad / g->kbw;
+    stream_format(g, ty);
+}
+
+sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int* variant, const char** name) {
     g->N = p->n; g->C = p->c; g->H = p->h; g->W = p->w; g->K = p->k; g->R = p->r; g->S = p->s;
     g->T = p->stride; g->P = p->pad; g->G = p->groups;
     g->Ho = (p->h + 2 * p->pad - p->r) / p->stride + 1;
     g->Wo = (p->w + 2 * p->pad - p->s) / p->stride + 1;
     g->Cg = p->c / p->groups;
     g->Kg = p->k / p->groups;
-    g->kbw = 32;  // set to 32*KL once the stage-2 variant is chosen (finish_geometry)
-    g->Kg_pad = (g->Kg + 31) / 32 * 32;
-    g->kblocks = g->Kg_pad / 32;
     g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
-    list_format(g->H, g->W, &g->th, &g->tiles, &g->idx_bytes, &g->cap);
-    g->num_lists = g->N * g->C * g->tiles;
+    choose_kernel(g, variant, name);
     dg->kdim = g->Cg * g->R * g->S;
     dg->kdim_pad = (dg->kdim + 31) / 32 * 32;
     dg->m_pad = (g->Kg + 127) / 128 * 128;
     const int64_t in_e = g->N * g->C * g->H * g->W, out_e = g->N * g->K * g->Ho * g->Wo;
     const int64_t w_e = g->G * g->Cg * g->R * g->S * g->Kg_pad;
-    const int64_t l_e = g->num_lists * g->cap;
+    const int64_t s_e = g->N * g->tiles * g->cap;  // 8-byte entries; indices are u32 inside a stream
     const int64_t d_e = g->G * dg->m_pad * dg->kdim_pad;
-    if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || l_e > kMaxElems || d_e > kMaxElems)
+    if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || s_e > kMaxElems || d_e > kMaxElems)
         return fail(SC_ERR_UNSUPPORTED, "a tensor has >= 2^31 elements");
     return SC_OK;
-}
-
-// Choose the stage-2 kernel (SC_FORCE_VARIANT env: -1 auto, 0 generic, id) and
-// fix the packed-weight k-block width it needs.
-void finish_geometry(Geometry* g, int* variant, const char** name) {
-    int force = -1;
-    if (const char* f = getenv("SC_FORCE_VARIANT")) force = atoi(f);
-    int kl = 1;
-    *variant = sc::gather_fast_select(*g, force, name, &kl);
-    if (*variant == 0) *name = "generic";
-    g->kbw = 32 * kl;
-    g->Kg_pad = (g->Kg + g->kbw - 1) / g->kbw * g->kbw;
-    g->kblocks = g->Kg_pad / g->kbw;
 }
 
 sc_status check_dev_ptr(const sc_plan_s* plan, const void* ptr, const char* name) {
@@ -148,9 +147,8 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->wpack);
     cudaFree(p->wdense);
     cudaFree(p->bias);
-    cudaFree(p->values);
-    cudaFree(p->idx);
-    cudaFree(p->counts);
+    cudaFree(p->entries);
+    cudaFree(p->offs);
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
     delete p;
@@ -207,7 +205,7 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     if (!plan) return fail(SC_ERR_OUT_OF_MEMORY, "host allocation failed");
     plan->params = *params;
     plan->device = device;
-    if ((st = make_geometry(params, &plan->g, &plan->dg)) != SC_OK) {
+    if ((st = make_geometry(params, &plan->g, &plan->dg, &plan->variant, &plan->variant_name)) != SC_OK) {
         delete plan;
         return st;
     }
@@ -217,7 +215,6 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         delete plan;
         return st;
     }
-    finish_geometry(&plan->g, &plan->variant, &plan->variant_name);
     const Geometry& g = plan->g;
     const DenseGeom& dg = plan->dg;
     cudaError_t e;
@@ -226,9 +223,8 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     if ((e = cudaMalloc(&plan->wpack, wbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->wdense, dbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
-        (e = cudaMalloc(&plan->values, sizeof(float) * g.num_lists * g.cap)) != cudaSuccess ||
-        (e = cudaMalloc(&plan->idx, (size_t)g.idx_bytes * g.num_lists * g.cap)) != cudaSuccess ||
-        (e = cudaMalloc(&plan->counts, sizeof(uint32_t) * g.num_lists)) != cudaSuccess) {
+        (e = cudaMalloc(&plan->entries, sizeof(uint2) * (g.N * g.tiles * g.cap + 2))) != cudaSuccess ||
+        (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess) {
         free_plan(plan);
         return cuda_fail(e, "sparse_conv_create: cudaMalloc");
     }
@@ -237,10 +233,9 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         e = cudaMemcpyAsync(plan->bias, d_bias, sizeof(float) * g.K, cudaMemcpyDeviceToDevice, st0);
     else
         e = cudaMemsetAsync(plan->bias, 0, sizeof(float) * g.K, st0);
-    // list slack is never interpreted (masked by counts) but is read by the
-    // register-tile kernel's 32-entry prefetch: keep it initialised
-    if (e == cudaSuccess) e = cudaMemsetAsync(plan->values, 0, sizeof(float) * g.num_lists * g.cap, st0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(plan->idx, 0, (size_t)g.idx_bytes * g.num_lists * g.cap, st0);
+    // stream slack is never interpreted, but the stage-2 bulk copies round
+    // piece boundaries to 16 bytes: keep the workspace initialised
+    if (e == cudaSuccess) e = cudaMemsetAsync(plan->entries, 0, sizeof(uint2) * (g.N * g.tiles * g.cap + 2), st0);
     if (e == cudaSuccess) e = sc::launch_pack_weights(g, d_weight, plan->wpack, st0);
     if (e == cudaSuccess) e = sc::launch_pack_dense(g, dg, d_weight, plan->wdense, st0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st0);
@@ -264,8 +259,7 @@ sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float* d_in, sc_str
     if (st != SC_OK) return st;
     if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
-    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->values, plan->idx, plan->counts,
-                                       (cudaStream_t)stream);
+    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->entries, plan->offs, (cudaStream_t)stream);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "compact launch");
 }
 
@@ -276,11 +270,11 @@ sc_status sparse_conv_gather(sc_plan plan, int64_t n, float* d_out, sc_stream_t 
     DeviceGuard guard(plan->device);
     cudaError_t e;
     if (plan->variant > 0)
-        e = sc::launch_gather_fast(plan->variant, plan->g, n, plan->values, plan->idx, plan->counts, plan->wpack,
-                                   plan->bias, d_out, (cudaStream_t)stream);
+        e = sc::launch_gather_fast(plan->variant, plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias,
+                                   d_out, (cudaStream_t)stream);
     else
-        e = sc::launch_gather_generic(plan->g, n, plan->values, plan->idx, plan->counts, plan->wpack, plan->bias,
-                                      d_out, (cudaStream_t)stream);
+        e = sc::launch_gather_generic(plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias, d_out,
+                                      (cudaStream_t)stream);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "gather launch");
 }
 
@@ -327,14 +321,15 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
 
 sc_status sparse_conv_lists(sc_plan plan, sc_lists_view* out) {
     if (!plan || !out) return fail(SC_ERR_INVALID_ARGUMENT, "NULL argument");
-    out->values = plan->values;
-    out->idx = plan->idx;
-    out->counts = plan->counts;
-    out->num_lists = plan->g.num_lists;
-    out->slot_capacity = plan->g.cap;
-    out->tiles_per_plane = plan->g.tiles;
-    out->row_tile_h = (int32_t)plan->g.th;
-    out->idx_bytes = (int32_t)plan->g.idx_bytes;
+    out->entries = reinterpret_cast<const uint32_t*>(plan->entries);
+    out->offsets = plan->offs;
+    out->tiles_per_image = plan->g.tiles;
+    out->stream_capacity = plan->g.cap;
+    out->channels = plan->g.C;
+    out->tile_rows = (int32_t)plan->g.ty;
+    out->window_rows = (int32_t)plan->g.nwr;
+    out->window_width = (int32_t)plan->g.W;
+    out->marker_code = (int32_t)plan->g.nwin;
     return SC_OK;
 }
 

@@ -1,128 +1,156 @@
-// Stage 1 of the sparse path: on-the-fly nonzero compaction.
+// Stage 1 of the sparse path: on-the-fly nonzero compaction into tile streams.
 //
 // ISC step 1: "we skip all the zero elements of the input data,
 // and store the non-zero values in a vector with their column and row
-// information".  List format: reading R9 (include/sparse_conv.h).
+// information".  Output format: reading R9 (include/sparse_conv.h,
+// DESIGN.md): one stream per (image n, output row-tile t) holding, for every
+// input channel c in order, a marker (c, NWIN) followed by the channel's
+// nonzeros inside the tile's input window as (value bits, window position),
+// ascending; offs[n][t][c] = index of channel c's marker, offs[..][C] = length.
+// The stream is exactly the instruction stream the stage-2 interpreter runs.
 //
-// Design: one warp per list.  A list is a contiguous
-// segment [start, start+len) of the flat NCHW array (TH whole rows of one
-// plane), generally not 16-byte aligned (e.g. 13x13 planes are 676 B).  The
-// warp reads the 16-byte-aligned float4s that cover the segment with
-// ld.global.nc.L1::no_allocate.v4 (LDG.E.128), masks the head/tail, and ranks
-// the nonzeros in scan order with four __ballot_sync + __popc per chunk.  All
-// of a short list's chunks are loaded before any is ranked, so every warp keeps
-// up to three 16-byte loads in flight.  The kernel is HBM-bound: it reads the
-// input once and writes nnz*(4 + idx) bytes plus one u32 count per list.
+// Design: one CTA of 8 warps per stream.
+//  pass 1: warp w counts the nonzeros of channels w, w+8, ... inside the
+//          window (a contiguous run of the flat NCHW array, generally not
+//          16-byte aligned: 16-byte-aligned LDG.128 over the covering float4s,
+//          masked head/tail, __ballot_sync + __popc);
+//  scan:   warp 0 turns the per-channel sizes (1 + count) into offsets
+//          (shuffle scan), written to global;
+//  pass 2: the same warps re-read their channels (L1/L2 hits) and write the
+//          marker and the entries at their ranks.
+// HBM traffic: the input once (+ the halo rows shared by neighbouring tiles)
+// and 8 bytes per written entry.
 #include "sc_internal.h"
 
 namespace sc {
 
-__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-}
+namespace {
 
-template <typename IdxT>
-__device__ __forceinline__ void rank_and_store(const float4 v, int64_t e0, int64_t start, int64_t end,
-                                               unsigned lane, uint32_t& base, float* __restrict__ vals,
-                                               IdxT* __restrict__ idx) {
-    const float q[4] = {v.x, v.y, v.z, v.w};
-    bool nz[4];
-    unsigned before = 0, total = 0;
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int64_t e = e0 + j;
-        nz[j] = (e >= start) && (e < end) && (q[j] != 0.0f);   // IEEE: -0.0 is zero
-        const unsigned b = __ballot_sync(0xffffffffu, nz[j]);
-        before += __popc(b & lt);
-        total += __popc(b);
-    }
-    uint32_t rank = base + before;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (nz[j]) {
-            vals[rank] = q[j];
-            idx[rank] = (IdxT)(e0 + j - start);
-            ++rank;
-        }
-    }
-    base += total;
-}
+__device__ __forceinline__ float4 ld_f4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-__device__ __forceinline__ float4 load_chunk(const float* __restrict__ in, int64_t e0, int64_t end,
-                                             int64_t total_elems) {
+// The covering float4 of element e0 (multiple of 4), zero outside [lo, hi)
+// and beyond the tensor end.
+__device__ __forceinline__ float4 load_chunk(const float* __restrict__ in, int64_t e0, int64_t hi, int64_t total) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 < end) {
-        if (e0 + 3 < total_elems) {
-            v = ld_stream_f4(in + e0);
-        } else {  // the very end of the tensor: scalar loads inside bounds only
+    if (e0 < hi) {
+        if (e0 + 3 < total) {
+            v = ld_f4(in + e0);
+        } else {
             v.x = in[e0];
-            if (e0 + 1 < total_elems) v.y = in[e0 + 1];
-            if (e0 + 2 < total_elems) v.z = in[e0 + 2];
+            if (e0 + 1 < total) v.y = in[e0 + 1];
+            if (e0 + 2 < total) v.z = in[e0 + 2];
         }
     }
     return v;
 }
 
-// MAXC > 0: lists span at most MAXC 128-float chunks (TH*W <= 256 -> 3);
-// MAXC == 0: generic loop for long rows (u16 indices).
-template <typename IdxT, int MAXC>
-__global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ in, int64_t num_lists,
-                                                      int64_t tiles, int64_t H, int64_t W, int64_t TH,
-                                                      int64_t cap, int64_t total_elems,
-                                                      float* __restrict__ values, IdxT* __restrict__ idx,
-                                                      uint32_t* __restrict__ counts) {
-    const unsigned lane = threadIdx.x & 31u;
-    const int64_t list = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (list >= num_lists) return;
-    const int64_t plane = list / tiles, tile = list - plane * tiles;
-    const int64_t row0 = tile * TH;
-    const int64_t rows = (H - row0 < TH) ? (H - row0) : TH;
-    const int64_t start = plane * H * W + row0 * W;
-    const int64_t end = start + rows * W;
-    const int64_t a0 = start & ~(int64_t)3;
-    float* vals = values + list * cap;
-    IdxT* ids = idx + list * cap;
-    uint32_t base = 0;
-    if constexpr (MAXC > 0) {
-        float4 v[MAXC];
+__device__ __forceinline__ unsigned nz_mask(float4 v, int64_t e0, int64_t lo, int64_t hi) {
+    const float q[4] = {v.x, v.y, v.z, v.w};
+    unsigned m = 0;
 #pragma unroll
-        for (int ch = 0; ch < MAXC; ++ch)
-            v[ch] = load_chunk(in, a0 + ch * 128 + 4 * lane, end, total_elems);
-#pragma unroll
-        for (int ch = 0; ch < MAXC; ++ch) {
-            if (a0 + ch * 128 < end)  // warp-uniform
-                rank_and_store<IdxT>(v[ch], a0 + ch * 128 + 4 * lane, start, end, lane, base, vals, ids);
-        }
-    } else {
-        for (int64_t b = a0; b < end; b += 128) {
-            const float4 v = load_chunk(in, b + 4 * lane, end, total_elems);
-            rank_and_store<IdxT>(v, b + 4 * lane, start, end, lane, base, vals, ids);
-        }
-    }
-    if (lane == 0) counts[list] = base;
+    for (int j = 0; j < 4; ++j)
+        if (e0 + j >= lo && e0 + j < hi && q[j] != 0.0f) m |= 1u << j;  // IEEE: -0.0 is zero
+    return m;
 }
 
-cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, float* values, void* idx,
-                           uint32_t* counts, cudaStream_t st) {
-    const int64_t num_lists = n * g.C * g.tiles;
-    const int threads = 256, wpb = threads / 32;
-    const int64_t blocks = (num_lists + wpb - 1) / wpb;
-    const int64_t total = n * g.C * g.H * g.W;
-    const bool short_lists = g.th * g.W <= 256;
-    if (g.idx_bytes == 1) {
-        compact_kernel<uint8_t, 3><<<(unsigned)blocks, threads, 0, st>>>(
-            in, num_lists, g.tiles, g.H, g.W, g.th, g.cap, total, values, (uint8_t*)idx, counts);
-    } else if (short_lists) {
-        compact_kernel<uint16_t, 3><<<(unsigned)blocks, threads, 0, st>>>(
-            in, num_lists, g.tiles, g.H, g.W, g.th, g.cap, total, values, (uint16_t*)idx, counts);
-    } else {
-        compact_kernel<uint16_t, 0><<<(unsigned)blocks, threads, 0, st>>>(
-            in, num_lists, g.tiles, g.H, g.W, g.th, g.cap, total, values, (uint16_t*)idx, counts);
+}  // namespace
+
+__global__ void __launch_bounds__(256) compact_streams_kernel(const float* __restrict__ in, int C, int H, int W,
+                                                              int TY, int tiles, int T, int P, int NWR, int NWIN,
+                                                              int64_t cap, int64_t total,
+                                                              uint2* __restrict__ entries,
+                                                              uint32_t* __restrict__ offs) {
+    extern __shared__ uint32_t cnt_s[];  // [C + 1]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int stream = blockIdx.x;
+    const int n = stream / tiles, t = stream - n * tiles;
+    const int i_lo = t * TY * T - P;
+    const int r0 = i_lo < 0 ? 0 : i_lo;
+    const int r1 = (i_lo + NWR < H) ? i_lo + NWR : H;
+    const int64_t seg = r1 > r0 ? (int64_t)(r1 - r0) * W : 0;
+    const unsigned lt = (1u << lane) - 1u;
+
+    // ---- pass 1: per-channel window counts
+    for (int c = warp; c < C; c += 8) {
+        const int64_t plane = ((int64_t)n * C + c) * H * W;
+        const int64_t lo = plane + (int64_t)r0 * W, hi = lo + seg;
+        unsigned cnt = 0;
+        for (int64_t b = lo & ~(int64_t)3; b < hi; b += 256) {  // two float4 per lane in flight
+            const float4 v0 = load_chunk(in, b + 4 * lane, hi, total);
+            const float4 v1 = load_chunk(in, b + 128 + 4 * lane, hi, total);
+            cnt += __popc(nz_mask(v0, b + 4 * lane, lo, hi)) + __popc(nz_mask(v1, b + 128 + 4 * lane, lo, hi));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) cnt_s[c] = cnt;
     }
+    __syncthreads();
+    // ---- exclusive scan of (1 + count): marker + entries per channel
+    if (warp == 0) {
+        uint32_t running = 0;
+        for (int base = 0; base < C; base += 32) {
+            const int c = base + lane;
+            const uint32_t v = c < C ? 1u + cnt_s[c] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (c < C) cnt_s[c] = running + incl - v;
+            running += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) cnt_s[C] = running;
+    }
+    __syncthreads();
+    uint32_t* of = offs + (int64_t)stream * (C + 1);
+    for (int c = threadIdx.x; c <= C; c += blockDim.x) of[c] = cnt_s[c];
+    // ---- pass 2: marker + entries
+    uint2* st = entries + (int64_t)stream * cap;
+    for (int c = warp; c < C; c += 8) {
+        const int64_t plane = ((int64_t)n * C + c) * H * W;
+        const int64_t lo = plane + (int64_t)r0 * W, hi = lo + seg;
+        const int64_t code0 = plane + (int64_t)i_lo * W;  // code = e - code0 = (i - i_lo)*W + j
+        uint32_t pos = cnt_s[c];
+        if (lane == 0) st[pos] = make_uint2((unsigned)c, (unsigned)NWIN);
+        ++pos;
+        for (int64_t b = lo & ~(int64_t)3; b < hi; b += 128) {
+            const int64_t e0 = b + 4 * lane;
+            const float4 v = load_chunk(in, e0, hi, total);
+            const unsigned m = nz_mask(v, e0, lo, hi);
+            const float q[4] = {v.x, v.y, v.z, v.w};
+            unsigned before = 0, tot = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned bal = __ballot_sync(0xffffffffu, (m >> j) & 1u);
+                before += __popc(bal & lt);
+                tot += __popc(bal);
+            }
+            uint32_t p = pos + before;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if ((m >> j) & 1u) {
+                    st[p] = make_uint2(__float_as_uint(q[j]), (unsigned)(e0 + j - code0));
+                    ++p;
+                }
+            }
+            pos += tot;
+        }
+    }
+}
+
+cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint2* entries, uint32_t* offs,
+                           cudaStream_t st) {
+    const int64_t streams = n * g.tiles;
+    const size_t smem = sizeof(uint32_t) * (g.C + 1);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(compact_streams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    compact_streams_kernel<<<(unsigned)streams, 256, smem, st>>>(
+        in, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.tiles, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
+        g.cap, n * g.C * g.H * g.W, entries, offs);
     return cudaGetLastError();
 }
 

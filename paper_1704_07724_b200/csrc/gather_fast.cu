@@ -7,39 +7,40 @@ namespace fast {
 #include "gather_variants.inc"
 template <class V>
 bool matches(const Geometry& g) {
-    return g.T == 1 && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1;
+    return g.T == 1 && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1 &&
+           (g.Cg + V::CH - 1) / V::CH <= 63;
 }
-#define SC_DECLARE(VV)                                                                                   \
-    cudaError_t launch_##VV(const Geometry& g, int64_t n, const float* values, const void* idx,          \
-                            const uint32_t* counts, const float* wpack, const float* bias, float* out,   \
-                            cudaStream_t st);
+#define SC_DECLARE(VV)                                                                                  \
+    cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,   \
+                            const float* wpack, const float* bias, float* out, cudaStream_t st);
 SC_GATHER_VARIANTS(SC_DECLARE)
 #undef SC_DECLARE
 }  // namespace fast
 
 // force < 0: first matching variant; force == 0: generic; force > 0: that
 // variant if it matches the geometry (else generic).
-int gather_fast_select(const Geometry& g, int force, const char** name, int* kl) {
+int gather_fast_select(const Geometry& g, int force, const char** name, int* kl, int* ty) {
     using namespace fast;
     *kl = 1;
-    if (g.idx_bytes != 1 || force == 0) return 0;
-#define SC_SELECT(VV)                                   \
+    *ty = (int)g.Ho;
+    if (force == 0) return 0;
+#define SC_SELECT(VV)                                       \
     if (matches<VV>(g) && (force < 0 || force == VV::ID)) { \
-        if (name) *name = VV::NAME;                     \
-        *kl = VV::KL;                                   \
-        return VV::ID;                                  \
+        if (name) *name = VV::NAME;                         \
+        *kl = VV::KL;                                       \
+        *ty = VV::TY;                                       \
+        return VV::ID;                                      \
     }
     SC_GATHER_VARIANTS(SC_SELECT)
 #undef SC_SELECT
     return 0;
 }
 
-cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const float* values, const void* idx,
-                               const uint32_t* counts, const float* wpack, const float* bias, float* out,
-                               cudaStream_t st) {
+cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
+                               const float* wpack, const float* bias, float* out, cudaStream_t st) {
     using namespace fast;
 #define SC_LAUNCH(VV) \
-    if (variant == VV::ID) return launch_##VV(g, n, values, idx, counts, wpack, bias, out, st);
+    if (variant == VV::ID) return launch_##VV(g, n, entries, offs, wpack, bias, out, st);
     SC_GATHER_VARIANTS(SC_LAUNCH)
 #undef SC_LAUNCH
     return cudaErrorInvalidValue;

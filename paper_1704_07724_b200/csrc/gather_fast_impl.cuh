@@ -10,18 +10,19 @@
 //    channels).  The packed weight slice wpack[g][kb][c0:c0+CH][R][S][KBW] of
 //    CH input channels is ONE contiguous run, streamed through a STAGES-deep
 //    shared-memory ring by 1-D TMA bulk copies (cp.async.bulk + mbarrier
-//    complete_tx); thread 0 refills a stage once all NW warps released it.
-//  * warp = one unit (image n, output rows [y0, y0+TY)); lane owns KL output
-//    channels (the paper's "4 floats of weights ... at one time", P:123,
-//    becomes 32*KL per warp).  The warp's tile acc[TY][NX] (f32x2 pairs) stays
-//    in registers for the whole reduction over input channels.
-//  * per input channel: the lane's R*S weights come from the ring (conflict-
-//    free LDS), the channel's nonzero list (stage-1 output, warp-uniform) is
-//    staged 32 entries at a time into a per-warp shared buffer keeping only
-//    entries inside the tile's input window; each entry is one indirect,
-//    warp-uniform branch (brx.idx.uni) into generated code that applies
-//    FFMA2/FFMA to exactly the accumulators the entry reaches
-//    (tools/gen_gather.py).
+//    complete_tx); thread 0 refills a stage once all active warps released it.
+//  * warp = one unit = one stage-1 tile stream (image n, output rows
+//    [y0, y0+TY)); lane owns KL output channels (the paper's "4 floats of
+//    weights ... at one time", becomes 32*KL per warp).  The warp's
+//    tile acc[TY][NX] (f32x2 pairs) stays in registers for the whole
+//    reduction over input channels.
+//  * the unit's stream (per channel: marker, then in-window nonzeros as
+//    (value, window position)) is cut into pieces at weight-chunk boundaries
+//    and every kPiece entries; each piece is bulk-copied (TMA, per-warp
+//    mbarrier) into a kSlots-deep per-warp shared ring, terminated with an EXIT
+//    entry and run by the generated threaded interpreter (tools/gen_gather.py):
+//    one brx.idx.uni per entry into code that applies FFMA2/FFMA to exactly the
+//    accumulators the entry reaches; markers reload the lane's weights.
 //  * epilogue (ISC step 3, "transpose temporary results"): registers ->
 //    per-warp shared buffer [k][pixels] -> contiguous NCHW runs, + bias,
 //    optional ReLU (Eq. 2).  One global write per output, no atomics;
@@ -34,25 +35,17 @@ namespace fast {
 
 #include "gather_variants.inc"
 
-constexpr int kSegRing = 32;  // list segments in flight per warp (cp.async ring, ~2 chunks)
-constexpr int kEntCap = 256;  // entries of the per-warp stream buffer
-
-// One prefetched list segment: count + first 32 values + first 32 u8 indices.
-struct __align__(16) SegSlot {
-    float v[32];
-    uint32_t i4[8];
-    uint32_t cnt;
-    uint32_t pad[3];
-};
+constexpr int kPiece = 254;  // max entries per piece (+ alignment slot + EXIT = 256)
+constexpr int kSlots = 3;    // pieces in flight per warp
 
 struct Args {
-    const float* values;
-    const void* idx;
-    const uint32_t* counts;
+    const uint2* entries;
+    const uint32_t* offs;
     const float* wpack;
     const float* bias;
     float* out;
-    int n, C, H, K, Cg, Kg, kblocks, Ho, th, tiles, cap, relu;
+    int n, C, H, K, Cg, Kg, kblocks, Ho, relu;
+    int64_t cap;
     int ytiles, units, ctas_per_kb;
 };
 
@@ -77,14 +70,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -96,32 +81,33 @@ template <class V>
 struct Smem {
     static constexpr int KBW = 32 * V::KL;
     static constexpr int kStageFloats = V::CH * V::R * V::S * KBW;
-    // epilogue rows per pass: KBW x (kER*WO) floats per warp ~ 8 KB
-    static constexpr int kERraw = (2048 / KBW) / V::WO;
+    // The epilogue reuses the warp's own piece slots (all its pieces have been
+    // consumed by then): KBW x kEpiStride floats must fit kSlots*(kPiece+2)*8 B.
+    static constexpr int kPieceFloats = kSlots * (kPiece + 2) * 2;
+    // One epilogue pass covers 32 output channels (KL passes).
+    static constexpr int kERraw = ((kPieceFloats / 32) - 1) / V::WO;
     static constexpr int kER = kERraw < 1 ? 1 : (kERraw > V::TY ? V::TY : kERraw);
-    static constexpr int kEpiStride = (kER * V::WO) | 1;                                        // odd
+    static constexpr int kEpiStride = (kER * V::WO) | 1;  // odd
+    static_assert(32 * kEpiStride <= kPieceFloats, "epilogue buffer does not fit the piece slots");
     static constexpr size_t ring = sizeof(float) * V::STAGES * kStageFloats;
-    static constexpr size_t bars = 16 * V::STAGES;
-    static constexpr size_t ent = sizeof(uint2) * V::NW * kEntCap;
-    static constexpr size_t seg = sizeof(SegSlot) * V::NW * kSegRing;
-    static constexpr size_t epi = sizeof(float) * V::NW * KBW * kEpiStride;
-    static constexpr size_t total = ring + bars + ent + seg + epi;
-    static_assert(total <= 227 * 1024, "shared memory budget of one CTA exceeded");
+    static constexpr size_t bars = 8 * (2 * V::STAGES + V::NW * kSlots);
+    static constexpr size_t bars_pad = (bars + 127) / 128 * 128;
+    static constexpr size_t pieces = sizeof(uint2) * V::NW * kSlots * (kPiece + 2);
+    static constexpr size_t total = ring + bars_pad + pieces;
+    static_assert(total * V::MINB <= 227 * 1024, "shared memory budget of the SM exceeded");
 };
 
-template <class V, typename IdxT>
-__global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a) {
+template <class V>
+__global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const Args a) {
     using SM = Smem<V>;
-    constexpr int R = V::R, RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO, W = V::W;
+    constexpr int RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO;
     constexpr int CH = V::CH, STAGES = V::STAGES, NW = V::NW, KBW = SM::KBW;
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring);
     uint64_t* empty = full + STAGES;
-    uint2* ent_all = reinterpret_cast<uint2*>(smem + SM::ring + SM::bars);
-    SegSlot* seg_all = reinterpret_cast<SegSlot*>(smem + SM::ring + SM::bars + SM::ent);
-    float* epi_all = reinterpret_cast<float*>(smem + SM::ring + SM::bars + SM::ent + SM::seg);
-    static_assert(sizeof(IdxT) == 1, "register-tile kernels read u8 list indices");
+    uint64_t* pbar_all = empty + STAGES;  // [NW][kSlots]
+    uint2* piece_all = reinterpret_cast<uint2*>(smem + SM::ring + SM::bars_pad);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cb = blockIdx.x % a.ctas_per_kb;
@@ -129,19 +115,16 @@ __global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a
     const int kb = gkb % a.kblocks, g = gkb / a.kblocks;
     const int unit = cb * NW + warp;
     const bool active = unit < a.units;
-    const int n = active ? unit / a.ytiles : 0;
-    const int y0 = active ? (unit % a.ytiles) * TY : 0;
+    const int nactive = (a.units - cb * NW) < NW ? (a.units - cb * NW) : NW;
     const int nchunks = (a.Cg + CH - 1) / CH;
     const float* wsrc = a.wpack + (size_t)gkb * a.Cg * RS * KBW;
 
-    // Warps without a unit (last CTA of a k-block) leave right after the
-    // barrier set-up; `empty` counts only the active warps of this CTA.
-    const int nactive = (a.units - cb * NW) < NW ? (a.units - cb * NW) : NW;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], (unsigned)nactive);
         }
+        for (int i = 0; i < NW * kSlots; ++i) mbar_init(&pbar_all[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -155,108 +138,82 @@ __global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a
     }
     if (!active) return;  // warp 0 is always active (every CTA has >= 1 unit)
 
-    // Lists overlapping the input window rows [y0 - P, y0 + TY - 1 + R - 1 - P].
-    int i_lo = y0 - V::P, i_hi = y0 + TY + R - 2 - V::P;
-    i_lo = i_lo < 0 ? 0 : i_lo;
-    i_hi = i_hi > a.H - 1 ? a.H - 1 : i_hi;
-    const int tl_lo = i_lo / a.th, nl = i_hi / a.th - tl_lo + 1;  // lists per channel (1..3)
+    const int n = unit / a.ytiles;
+    const int y0 = (unit % a.ytiles) * TY;
+    const int64_t stream = (int64_t)unit;  // = n * tiles + tile (ytiles == tiles)
+    const uint2* sbase = a.entries + stream * a.cap;
+    const uint32_t* of = a.offs + stream * (a.C + 1) + (int64_t)g * a.Cg;  // of[cl] = marker of channel g*Cg+cl
+    uint64_t* pbar = pbar_all + warp * kSlots;
+    uint2* pieces = piece_all + warp * kSlots * (kPiece + 2);
 
     unsigned long long acc[TY][NX];  // f32x2 bit patterns, low word = first element
 #pragma unroll
     for (int ty = 0; ty < TY; ++ty)
 #pragma unroll
         for (int m = 0; m < NX; ++m) acc[ty][m] = 0ull;
-
-    uint2* ent = ent_all + warp * kEntCap;
-    const unsigned ent_s = smem_u32(ent);
-    const float* vbase = a.values;
-    const IdxT* ibase = reinterpret_cast<const IdxT*>(a.idx);
-    // list id of channel cl, list l = (n*C + g*Cg + cl)*tiles + tl_lo + l
-    const int list0 = (n * a.C + g * a.Cg) * a.tiles + tl_lo;
-
-    // Segment s = (channel s / nl, list s % nl).  A per-warp ring of kSegRing
-    // shared-memory slots receives, by cp.async (no registers held while in
-    // flight), the count and the first 32 entries of each segment, two weight
-    // chunks ahead of use.  The first 32 slots of a list are read regardless
-    // of its count (slack is zero-initialised at plan creation and masked).
-    const int nseg = a.Cg * nl;
-    SegSlot* segring = seg_all + warp * kSegRing;
-    const int vlanes = a.cap < 32 ? a.cap : 32;
-    auto seg_list = [&](int s) -> int {
-        const int cl = nl == 1 ? s : s / nl;
-        return list0 + cl * a.tiles + (s - cl * nl);
-    };
-    auto issue = [&](int s) {
-        if (active && s < nseg) {
-            SegSlot* sl = segring + (s % kSegRing);
-            const size_t list = (size_t)seg_list(s);
-            if (lane < vlanes) cp_async4(&sl->v[lane], vbase + list * a.cap + lane);
-            if (lane < (vlanes + 3) / 4)
-                cp_async4(&sl->i4[lane], reinterpret_cast<const uint8_t*>(ibase) + list * a.cap + 4 * lane);
-            if (lane == 31) cp_async4(&sl->cnt, a.counts + list);
-        }
-        cp_async_commit();
-    };
-#pragma unroll 1
-    for (int d = 0; d < kSegRing; ++d) issue(d);
-
     unsigned long long wp[V::NWOPS];
 #pragma unroll
     for (int i = 0; i < V::NWOPS; ++i) wp[i] = 0ull;
-    int s = 0;  // next segment to stage
+
+    // Chunk boundaries bnd(q) = of[min(q*CH, Cg)], q <= nchunks (<= 63), held
+    // two per lane and broadcast with shuffles.
+    const uint32_t bnd0 = __ldg(&of[(lane * CH < a.Cg) ? lane * CH : a.Cg]);
+    const uint32_t bnd1 = __ldg(&of[((lane + 32) * CH < a.Cg) ? (lane + 32) * CH : a.Cg]);
+    auto bnd = [&](int q) -> uint32_t {
+        const uint32_t v0 = __shfl_sync(0xffffffffu, bnd0, q & 31);
+        const uint32_t v1 = __shfl_sync(0xffffffffu, bnd1, q & 31);
+        return q < 32 ? v0 : v1;
+    };
+    // Piece sequence: the range [bnd(0), bnd(nchunks)) cut at chunk
+    // boundaries and every kPiece entries.  Issue and consume cursors walk it
+    // identically; lane 0 issues the bulk copies.
+    int iq = 0;                 // issue cursor: chunk
+    uint32_t ia = bnd(0);       // issue cursor: next entry
+    uint32_t iend = bnd(1);
+    int issued = 0;
+    auto issue_next = [&]() {
+        if (iq >= nchunks) return;
+        const uint32_t b = (ia + kPiece < iend) ? ia + kPiece : iend;
+        const int slot = issued % kSlots;
+        if (lane == 0) {
+            const uint32_t a2 = ia & ~1u;
+            const unsigned bytes = ((b - a2) * 8u + 15u) & ~15u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // EXIT write -> TMA overwrite
+            mbar_expect_tx(&pbar[slot], bytes);
+            tma_bulk_g2s(pieces + slot * (kPiece + 2), sbase + a2, bytes, &pbar[slot]);
+        }
+        ++issued;
+        ia = b;
+        if (ia == iend) {
+            ++iq;
+            iend = bnd(iq + 1 <= nchunks ? iq + 1 : nchunks);
+        }
+    };
+#pragma unroll 1
+    for (int i = 0; i < kSlots; ++i) issue_next();
+
+    int consumed = 0;
+    uint32_t ca = bnd(0);  // consume cursor
 #pragma unroll 1
     for (int ch = 0; ch < nchunks; ++ch) {
         const int st = ch % STAGES;
-        const int cc_n = (a.Cg - ch * CH) < CH ? (a.Cg - ch * CH) : CH;
+        const uint32_t chunk_end = bnd(ch + 1);
         const unsigned wlane = smem_u32(ring + st * SM::kStageFloats) + lane * 4 * V::KL;
-        if (active) {
-            // Stage this chunk's entry stream: per channel a LOADW entry, then
-            // its in-window nonzeros (ascending), finally EXIT.
-            int base = 0;
+        const unsigned cbase = (unsigned)(g * a.Cg + ch * CH);
+        mbar_wait(&full[st], (ch / STAGES) & 1);  // this chunk's weights have landed
 #pragma unroll 1
-            for (int cc = 0; cc < cc_n; ++cc) {
-                if (lane == 0) ent[base] = make_uint2((unsigned)(cc * RS * KBW * 4), (unsigned)V::LOADW);
-                ++base;
-#pragma unroll 1
-                for (int l = 0; l < nl; ++l, ++s) {
-                    cp_async_wait<kSegRing - 1>();  // segment s has landed
-                    __syncwarp();
-                    SegSlot* sl = segring + (s % kSegRing);
-                    const uint32_t cnt = sl->cnt;
-                    float v0 = sl->v[lane];
-                    int i0 = (int)((sl->i4[lane >> 2] >> (8 * (lane & 3))) & 0xffu);
-                    __syncwarp();
-                    issue(s + kSegRing);  // refill this slot
-                    const int off = ((tl_lo + l) * a.th - (y0 - V::P)) * W;
-#pragma unroll 1
-                    for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
-                        if (e0 > 0) {  // long list (dense input): synchronous loads
-                            const int list = seg_list(s);
-                            const bool ok = e0 + lane < cnt;
-                            v0 = ok ? vbase[(size_t)list * a.cap + e0 + lane] : 0.f;
-                            i0 = ok ? (int)ibase[(size_t)list * a.cap + e0 + lane] : 0;
-                        }
-                        const int cs = i0 + off;
-                        const bool inwin = (e0 + lane < cnt) && cs >= 0 && cs < V::NCASES;
-                        const unsigned bal = __ballot_sync(0xffffffffu, inwin);
-                        if (base + 32 + 2 > kEntCap) {  // stream full: run what we have
-                            if (lane == 0) ent[base] = make_uint2(0u, (unsigned)V::EXIT);
-                            __syncwarp();
-                            mbar_wait(&full[st], (ch / STAGES) & 1);
-                            V::run(acc, wp, ent_s, wlane);
-                            __syncwarp();
-                            base = 0;
-                        }
-                        const int rank = __popc(bal & ((1u << lane) - 1u));
-                        if (inwin) ent[base + rank] = make_uint2(__float_as_uint(v0), (unsigned)cs);
-                        base += __popc(bal);
-                    }
-                }
-            }
-            if (lane == 0) ent[base] = make_uint2(0u, (unsigned)V::EXIT);
+        while (ca < chunk_end) {
+            const uint32_t b = (ca + kPiece < chunk_end) ? ca + kPiece : chunk_end;
+            const int slot = consumed % kSlots;
+            mbar_wait(&pbar[slot], (consumed / kSlots) & 1);
+            uint2* p = pieces + slot * (kPiece + 2) + (ca & 1u);
+            if (lane == 0) p[b - ca] = make_uint2(0u, (unsigned)V::EXIT);
             __syncwarp();
-            mbar_wait(&full[st], (ch / STAGES) & 1);  // this chunk's weights have landed
-            V::run(acc, wp, ent_s, wlane);
+            V::run(acc, wp, smem_u32(p), wlane, cbase);
+            __syncwarp();
+            ++consumed;
+            ca = b;
+            issue_next();  // refill the slot just consumed
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -273,11 +230,33 @@ __global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a
         }
     }
 
-    if (!active) return;
     // Epilogue: registers -> smem [k][rows*WO] -> contiguous NCHW runs.
     constexpr int ER = SM::kER, ES = SM::kEpiStride;
-    float* epi = epi_all + warp * KBW * ES;
+    float* epi = reinterpret_cast<float*>(pieces);  // this warp's slots are idle now
     const int kloc = kb * KBW;
+    // bias (+ ReLU, Eq. 2) in registers: lane owns channels kloc + KL*lane + {0, KL-1} (KL=2)
+    // or kloc + lane (KL=1)
+    {
+        const int k0 = kloc + V::KL * lane;
+        const float b0 = k0 < a.Kg ? __ldg(&a.bias[g * a.Kg + k0]) : 0.f;
+        const float b1 = (V::KL == 2 && k0 + 1 < a.Kg) ? __ldg(&a.bias[g * a.Kg + k0 + 1]) : b0;
+#pragma unroll
+        for (int ty = 0; ty < TY; ++ty)
+#pragma unroll
+            for (int m = 0; m < NX; ++m) {
+                float lo = __uint_as_float((unsigned)acc[ty][m]) + b0;
+                float hi = __uint_as_float((unsigned)(acc[ty][m] >> 32)) + b1;
+                if (a.relu) {
+                    lo = fmaxf(lo, 0.f);
+                    hi = fmaxf(hi, 0.f);
+                }
+                acc[ty][m] = (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+            }
+    }
+    const int krows = (a.Kg - kloc) < KBW ? (a.Kg - kloc) : KBW;  // valid output channels of this block
+    // KL=2: one pass per pair half (h=0: k = 2*lane, h=1: k = 2*lane+1)
+#pragma unroll
+    for (int h = 0; h < V::KL; ++h)
 #pragma unroll
     for (int r0 = 0; r0 < TY; r0 += ER) {
 #pragma unroll
@@ -287,9 +266,8 @@ __global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a
                 for (int m = 0; m < NX; ++m) {
                     const float lo = __uint_as_float((unsigned)acc[r0 + rr][m]);
                     const float hi = __uint_as_float((unsigned)(acc[r0 + rr][m] >> 32));
-                    if constexpr (V::KL == 2) {  // (k = 2*lane, 2*lane+1) of pixel x = m
-                        epi[(2 * lane) * ES + rr * WO + m] = lo;
-                        epi[(2 * lane + 1) * ES + rr * WO + m] = hi;
+                    if constexpr (V::KL == 2) {  // channel 2*lane+h of pixel x = m
+                        epi[lane * ES + rr * WO + m] = h ? hi : lo;
                     } else {                     // (x = 2m, 2m+1) of channel k = lane
                         epi[lane * ES + rr * WO + 2 * m] = lo;
                         if (2 * m + 1 < WO) epi[lane * ES + rr * WO + 2 * m + 1] = hi;
@@ -301,38 +279,37 @@ __global__ void __launch_bounds__(V::NW * 32, 1) gather_fast_kernel(const Args a
         int rows = TY - r0 < ER ? TY - r0 : ER;
         if (y0 + r0 + rows > a.Ho) rows = a.Ho - (y0 + r0);
         if (rows > 0) {
+            // flattened (channel row kk, pixel p) loop: 32 consecutive elements per step
             const int len = rows * WO;
-#pragma unroll 1
-            for (int kk = 0; kk < KBW; ++kk) {
-                const int k = kloc + kk;
-                if (k >= a.Kg) break;
-                const int kglob = g * a.Kg + k;
-                const float b = __ldg(&a.bias[kglob]);
-                float* dst = a.out + ((size_t)(n * a.K + kglob) * a.Ho + y0 + r0) * WO;
-                for (int p = lane; p < len; p += 32) {
-                    float o = epi[kk * ES + p] + b;
-                    if (a.relu) o = fmaxf(o, 0.f);
-                    dst[p] = o;
-                }
+            const int nrows = V::KL == 2 ? (krows - h + 1) / 2 : krows;
+            const int total = nrows * len;
+            float* dst0 = a.out + ((size_t)(n * a.K + g * a.Kg + kloc + h) * a.Ho + y0 + r0) * WO;
+            const size_t kstride = (size_t)a.Ho * WO * V::KL;
+#pragma unroll 4
+            for (int idx = lane; idx < total; idx += 32) {
+                const int kk = idx / len, p = idx - kk * len;
+                dst0[kk * kstride + p] = epi[kk * ES + p];
             }
         }
         __syncwarp();
     }
 }
 
-template <class V, typename IdxT>
-cudaError_t launch_v(const Geometry& g, int64_t n, const float* values, const void* idx, const uint32_t* counts,
-                     const float* wpack, const float* bias, float* out, cudaStream_t st) {
+template <class V>
+cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs, const float* wpack,
+                     const float* bias, float* out, cudaStream_t st) {
+    if (g.ty != V::TY || g.tiles != (g.Ho + V::TY - 1) / V::TY || (g.Cg + V::CH - 1) / V::CH > 63)
+        return cudaErrorInvalidValue;
     Args a;
-    a.values = values; a.idx = idx; a.counts = counts; a.wpack = wpack; a.bias = bias; a.out = out;
+    a.entries = entries; a.offs = offs; a.wpack = wpack; a.bias = bias; a.out = out;
     a.n = (int)n; a.C = (int)g.C; a.H = (int)g.H; a.K = (int)g.K; a.Cg = (int)g.Cg; a.Kg = (int)g.Kg;
-    a.kblocks = (int)g.kblocks; a.Ho = (int)g.Ho; a.th = (int)g.th; a.tiles = (int)g.tiles; a.cap = (int)g.cap;
-    a.relu = g.relu ? 1 : 0;
-    a.ytiles = (int)((g.Ho + V::TY - 1) / V::TY);
+    a.kblocks = (int)g.kblocks; a.Ho = (int)g.Ho; a.relu = g.relu ? 1 : 0;
+    a.cap = g.cap;
+    a.ytiles = (int)g.tiles;
     a.units = (int)n * a.ytiles;
     a.ctas_per_kb = (a.units + V::NW - 1) / V::NW;
     const size_t smem = Smem<V>::total;
-    auto kern = gather_fast_kernel<V, IdxT>;
+    auto kern = gather_fast_kernel<V>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
@@ -344,13 +321,12 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const float* values, const vo
 }  // namespace sc
 
 // Each gather_fast_vN.cu instantiates one variant (parallel compilation).
-#define SC_INSTANTIATE_VARIANT(VV)                                                                         \
-    namespace sc {                                                                                         \
-    namespace fast {                                                                                       \
-    cudaError_t launch_##VV(const Geometry& g, int64_t n, const float* values, const void* idx,            \
-                            const uint32_t* counts, const float* wpack, const float* bias, float* out,     \
-                            cudaStream_t st) {                                                             \
-        return launch_v<VV, uint8_t>(g, n, values, idx, counts, wpack, bias, out, st);                    \
-    }                                                                                                      \
-    }                                                                                                      \
+#define SC_INSTANTIATE_VARIANT(VV)                                                                          \
+    namespace sc {                                                                                          \
+    namespace fast {                                                                                        \
+    cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,       \
+                            const float* wpack, const float* bias, float* out, cudaStream_t st) {           \
+        return launch_v<VV>(g, n, entries, offs, wpack, bias, out, st);                                     \
+    }                                                                                                       \
+    }                                                                                                       \
     }

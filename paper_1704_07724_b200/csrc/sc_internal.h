@@ -16,8 +16,9 @@ struct Geometry {
     int64_t kbw;            // k-block width of the packed weights: 32 * KL of the stage-2 kernel
     int64_t Kg_pad;         // Kg rounded up to kbw
     int64_t kblocks;        // Kg_pad / kbw
-    // stage-1 list format (reading R9)
-    int64_t th, tiles, cap, idx_bytes, num_lists;  // num_lists for N images
+    // stage-1 tile streams (reading R9): row-tile height, tiles per image,
+    // window rows / positions, capacity (entries) of one stream
+    int64_t ty, tiles, nwr, nwin, cap;
     bool relu;
 };
 
@@ -32,18 +33,18 @@ struct DenseGeom {
 cudaError_t launch_pack_weights(const Geometry& g, const float* w, float* wpack, cudaStream_t st);
 cudaError_t launch_pack_dense(const Geometry& g, const DenseGeom& dg, const float* w, float* wdense,
                               cudaStream_t st);
-cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, float* values, void* idx,
-                           uint32_t* counts, cudaStream_t st);
-cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const float* values, const void* idx,
-                                  const uint32_t* counts, const float* wpack, const float* bias,
-                                  float* out, cudaStream_t st);
+cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint2* entries, uint32_t* offs,
+                           cudaStream_t st);
+cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
+                                  const float* wpack, const float* bias, float* out, cudaStream_t st);
 
 // Shape-specialised stage-2 kernels (gather_fast.cu).  `select` returns a
-// variant id > 0 if one applies to the geometry, else 0.
-int gather_fast_select(const Geometry& g, int force, const char** name, int* kl);
-cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const float* values,
-                               const void* idx, const uint32_t* counts, const float* wpack,
-                               const float* bias, float* out, cudaStream_t st);
+// variant id > 0 (and its lanes-per-channel KL and tile height TY) if one
+// applies to the geometry, else 0.
+int gather_fast_select(const Geometry& g, int force, const char** name, int* kl, int* ty);
+cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries,
+                               const uint32_t* offs, const float* wpack, const float* bias, float* out,
+                               cudaStream_t st);
 
 // Dense tcgen05 TF32 implicit GEMM (dense_tc.cu).
 cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in,

@@ -37,9 +37,9 @@ class ConvParams(ctypes.Structure):
 
 
 class ListsView(ctypes.Structure):
-    _fields_ = [("values", ctypes.c_void_p), ("idx", ctypes.c_void_p), ("counts", ctypes.c_void_p),
-                ("num_lists", ctypes.c_int64), ("slot_capacity", ctypes.c_int64),
-                ("tiles_per_plane", ctypes.c_int64), ("row_tile_h", ctypes.c_int32), ("idx_bytes", ctypes.c_int32)]
+    _fields_ = [("entries", ctypes.c_void_p), ("offsets", ctypes.c_void_p), ("tiles_per_image", ctypes.c_int64),
+                ("stream_capacity", ctypes.c_int64), ("channels", ctypes.c_int64), ("tile_rows", ctypes.c_int32),
+                ("window_rows", ctypes.c_int32), ("window_width", ctypes.c_int32), ("marker_code", ctypes.c_int32)]
 
 
 _lib = None
@@ -180,19 +180,17 @@ class SparseConv:
         return out
 
     def lists(self, n):
-        """Device views of the list workspace for the first n images:
-        dict(values [L][cap] f32, idx [L][cap] u8/u16, counts [L] i32-view of u32, th, tiles, cap)."""
+        """Device views (int32 bit patterns of the u32 words) of the stage-1
+        tile streams of the first n images: dict(entries [n][tiles][cap][2],
+        offs [n][tiles][C+1], ty, tiles, nwr, nwin, cap)."""
         v = ListsView()
         _check(lib().sparse_conv_lists(self._plan, ctypes.byref(v)))
-        nl = n * self.in_shape[0] * v.tiles_per_plane
-        cap = v.slot_capacity
+        tiles, cap, c = v.tiles_per_image, v.stream_capacity, v.channels
         with torch.cuda.device(self.device):
-            values = torch.as_tensor(_DevArray(v.values, (nl, cap), "<f4"), device=self.device)
-            idx = torch.as_tensor(_DevArray(v.idx, (nl, cap), "|u1" if v.idx_bytes == 1 else "<i2"),
-                                  device=self.device)
-            counts = torch.as_tensor(_DevArray(v.counts, (nl,), "<i4"), device=self.device)
-        return dict(values=values, idx=idx, counts=counts, th=v.row_tile_h, tiles=v.tiles_per_plane, cap=cap,
-                    idx_bytes=v.idx_bytes)
+            entries = torch.as_tensor(_DevArray(v.entries, (n, tiles, cap, 2), "<i4"), device=self.device)
+            offs = torch.as_tensor(_DevArray(v.offsets, (n, tiles, c + 1), "<i4"), device=self.device)
+        return dict(entries=entries, offs=offs, ty=v.tile_rows, tiles=tiles, nwr=v.window_rows,
+                    nwin=v.marker_code, cap=cap)
 
     @property
     def variant(self):

@@ -32,18 +32,19 @@ def make_conv(sc, shp, w, b, relu=False, max_batch=None):
 
 
 def check_lists(conv, x, n):
-    """Bit-exact comparison of the GPU list workspace with oracle.compact."""
-    ref = oracle.compact(x[:n])
+    """Bit-exact comparison of the GPU stage-1 tile streams with
+    oracle.compact_streams for the plan's tile height (entries beyond each
+    stream's length are never compared)."""
+    p = conv.params
     got = conv.lists(n)
-    assert got["th"] == ref["th"] and got["tiles"] == ref["tiles"] and got["cap"] == ref["cap"]
-    counts = got["counts"].cpu().numpy().view(np.uint32)
-    assert np.array_equal(counts, ref["counts"])
-    cap = ref["cap"]
-    valid = np.arange(cap)[None, :] < ref["counts"][:, None]
-    gv = got["values"].cpu().numpy().view(np.uint32)
-    gi = got["idx"].cpu().numpy().view(ref["idx"].dtype)
-    assert np.array_equal(np.where(valid, gv, 0), np.where(valid, ref["values"].view(np.uint32), 0))
-    assert np.array_equal(np.where(valid, gi, 0), np.where(valid, ref["idx"], 0))
+    ref = oracle.compact_streams(x[:n], p.r, p.stride, p.pad, got["ty"])
+    assert (got["tiles"], got["nwr"], got["nwin"], got["cap"]) == (ref["tiles"], ref["nwr"], ref["nwin"], ref["cap"])
+    offs = got["offs"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(offs, ref["offs"])
+    length = ref["offs"][:, :, -1]
+    valid = np.arange(ref["cap"])[None, None, :] < length[:, :, None]
+    ge = got["entries"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref["entries"], 0))
 
 
 def check_conv(got, x, w, b, shp, relu=False, images=None):
@@ -140,7 +141,7 @@ def test_zero_input_gives_bias(sc, cfg):
     out = conv.forward(x).cpu().numpy()
     assert np.array_equal(out, np.broadcast_to(b[None, :, None, None], out.shape))
     lists = conv.lists(2)
-    assert int(lists["counts"].sum()) == 0
+    assert int(lists["offs"][:, :, -1].sum()) == 2 * shp.c * lists["tiles"]   # markers only
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4a"])
@@ -177,7 +178,8 @@ def test_subnormal_inputs_count_as_nonzero(sc):
     conv.compact(torch.from_numpy(x).to(DEV))
     torch.cuda.synchronize()
     check_lists(conv, x, 1)
-    assert int(conv.lists(1)["counts"].sum()) == 1
+    st = conv.lists(1)
+    assert int(st["offs"][0, :, -1].sum()) == shp.c * st["tiles"] + 1   # markers + the subnormal
     ws = np.full_like(w, 2.0 ** 100)
     conv2 = make_conv(sc, shp, ws, None)
     out = conv2.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()

@@ -110,10 +110,14 @@ def test_hand_worked_example():
     assert np.array_equal(out.reshape(-1), np.array(g["output"], dtype=np.float64))
     assert oracle.exact_nonzero_macs(x, 1, 3, 3, 1, 1) == int(g["exact_macs"][0])
     assert oracle.dense_macs(1, 1, 3, 3, 1, 3, 3, 1, 1) == int(g["dense_macs"][0])
-    lists = oracle.compact(x)
-    assert int(lists["counts"][0]) == int(g["list_count"][0])
-    assert np.array_equal(lists["values"][0, :2], np.array(g["list_values"], dtype=np.float32))
-    assert np.array_equal(lists["idx"][0, :2], np.array(g["list_idx"], dtype=np.uint8))
+    st = oracle.compact_streams(x, 3, 1, 1, 3)
+    assert st["tiles"] == 1 and st["nwin"] == 15
+    offs = st["offs"][0, 0]
+    assert list(offs) == [int(v) for v in g["stream_offs"]]
+    e = st["entries"][0, 0, :3]
+    a = [int(g["stream_a"][0])] + [int(np.float32(v).view(np.uint32)) for v in g["stream_a"][1:]]
+    assert list(e[:, 0]) == a
+    assert list(e[:, 1]) == [int(v) for v in g["stream_b"]]
 
 
 def _torch_ref(x, w, b, stride, pad, groups):
@@ -268,37 +272,70 @@ def test_mac_conservation_at_zero_sparsity(table2):
 
 
 # ---------------------------------------------------------------------------
-# compaction (ISC step 1)
+# compaction (ISC step 1) in the tile-stream format
 # ---------------------------------------------------------------------------
-def test_list_format():
-    assert oracle.list_format(13, 13) == (13, 1, 1, 176)
-    assert oracle.list_format(27, 27) == (9, 3, 1, 256)
-    assert oracle.list_format(28, 28) == (9, 4, 1, 256)
-    assert oracle.list_format(12, 12) == (12, 1, 1, 144)
-    assert oracle.list_format(3, 300) == (1, 3, 2, 304)
-    assert oracle.list_format(16, 16) == (16, 1, 1, 256)
+def test_stream_format():
+    # (c, h, w, r, stride, pad, ty, ho) -> (tiles, nwr, nwin, cap)
+    assert oracle.stream_format(256, 13, 13, 3, 1, 1, 13, 13) == (1, 15, 195, 256 * (1 + 13 * 13))
+    assert oracle.stream_format(256, 13, 13, 3, 1, 1, 7, 13) == (2, 9, 117, 256 * (1 + 9 * 13))
+    assert oracle.stream_format(20, 11, 11, 5, 2, 1, 5, 5) == (1, 13, 143, 20 * (1 + 11 * 11))
+    assert oracle.stream_format(3, 5, 5, 1, 1, 0, 2, 5) == (3, 2, 10, 3 * 11 + 1)
 
 
-@pytest.mark.parametrize("shape", [(2, 3, 13, 13), (1, 2, 28, 28), (2, 2, 27, 27), (1, 1, 5, 300), (3, 2, 1, 1)])
-def test_compact_roundtrip_counts_and_order(shape):
-    rng = np.random.default_rng(sum(shape))
-    x = (np.abs(rng.standard_normal(shape)) * (rng.random(shape) > 0.9)).astype(np.float32)
-    lists = oracle.compact(x)
-    th, tiles = lists["th"], lists["tiles"]
-    n, c, h, w = shape
-    for l in range(n * c * tiles):
-        plane, tile = divmod(l, tiles)
-        seg = x.reshape(n * c, h * w)[plane, tile * th * w: min(h, (tile + 1) * th) * w]
-        cnt = int(lists["counts"][l])
-        assert cnt == np.count_nonzero(seg)
-        idx = lists["idx"][l, :cnt].astype(np.int64)
-        assert np.all(np.diff(idx) > 0)
-        assert np.array_equal(lists["values"][l, :cnt].view(np.uint32), seg[idx].view(np.uint32))
-    back = oracle.decompress(lists, shape)
-    assert np.array_equal(back.view(np.uint32), x.view(np.uint32))
+def _window_entries_reference(x, r, stride, pad, ty):
+    """Independent construction with numpy (np.nonzero) of what every stream
+    must contain: per (n, tile, c) the ascending nonzeros inside the window."""
+    n, c, h, w = x.shape
+    ho = (h + 2 * pad - r) // stride + 1
+    tiles = -(-ho // ty)
+    nwr = (ty - 1) * stride + r
+    out = {}
+    for ni in range(n):
+        for t in range(tiles):
+            i_lo = t * ty * stride - pad
+            rows = [i for i in range(i_lo, i_lo + nwr) if 0 <= i < h]
+            for ci in range(c):
+                if rows:
+                    sub = x[ni, ci, rows[0]:rows[-1] + 1]
+                    ii, jj = np.nonzero(sub)          # row-major ascending
+                    vals = sub[ii, jj].view(np.uint32)
+                    codes = (ii + rows[0] - i_lo) * w + jj
+                else:
+                    vals = codes = np.zeros(0, np.int64)
+                out[(ni, t, ci)] = (vals.astype(np.uint32), codes.astype(np.uint32))
+    return out, tiles, nwr * w
 
 
-def test_compact_zero_semantics():
+@pytest.mark.parametrize("shape,r,stride,pad,ty", [((2, 3, 13, 13), 3, 1, 1, 13), ((2, 3, 13, 13), 3, 1, 1, 7),
+                                                  ((1, 2, 28, 28), 3, 1, 1, 3), ((2, 2, 27, 27), 5, 1, 2, 2),
+                                                  ((1, 4, 11, 11), 5, 2, 1, 5), ((2, 3, 7, 7), 1, 1, 0, 3),
+                                                  ((3, 2, 1, 1), 1, 1, 0, 1)])
+def test_compact_streams_against_numpy_and_roundtrip(shape, r, stride, pad, ty):
+    rng = np.random.default_rng(sum(shape) + ty)
+    x = (np.abs(rng.standard_normal(shape)) * (rng.random(shape) > 0.85)).astype(np.float32)
+    st = oracle.compact_streams(x, r, stride, pad, ty)
+    ref, tiles, nwin = _window_entries_reference(x, r, stride, pad, ty)
+    assert st["tiles"] == tiles and st["nwin"] == nwin
+    n, c = shape[:2]
+    for ni in range(n):
+        for t in range(tiles):
+            of = st["offs"][ni, t].astype(np.int64)
+            e = st["entries"][ni, t]
+            for ci in range(c):
+                a, b = of[ci], of[ci + 1]
+                assert e[a, 0] == ci and e[a, 1] == nwin
+                vals, codes = ref[(ni, t, ci)]
+                assert np.array_equal(e[a + 1:b, 0], vals)
+                assert np.array_equal(e[a + 1:b, 1], codes)
+    back = oracle.decompress_streams(st, shape, stride, pad)
+    covered = np.zeros(shape[2], bool)
+    for t in range(tiles):
+        lo = t * ty * stride - pad
+        covered[max(lo, 0):max(min(lo + (ty - 1) * stride + r, shape[2]), 0)] = True
+    assert np.array_equal(back[:, :, covered].view(np.uint32), x[:, :, covered].view(np.uint32))
+
+
+def test_compact_streams_zero_semantics():
     """R7: IEEE compare x != 0.0f: -0.0 is zero; subnormals, NaN, Inf are not."""
     x = np.zeros((1, 1, 2, 4), np.float32)
     x[0, 0, 0, 0] = -0.0
@@ -306,10 +343,11 @@ def test_compact_zero_semantics():
     x[0, 0, 0, 2] = np.nan
     x[0, 0, 1, 0] = np.inf
     x[0, 0, 1, 3] = -2.5
-    lists = oracle.compact(x)
-    assert int(lists["counts"][0]) == 4
-    assert list(lists["idx"][0, :4]) == [1, 2, 4, 7]
-    assert lists["values"][0, 0].view(np.uint32) == np.float32(1e-45).view(np.uint32)
+    st = oracle.compact_streams(x, 1, 1, 0, 2)
+    e = st["entries"][0, 0]
+    assert int(st["offs"][0, 0, 1]) == 5
+    assert list(e[1:5, 1]) == [1, 2, 4, 7]
+    assert e[1, 0] == np.float32(1e-45).view(np.uint32)
 
 
 # ---------------------------------------------------------------------------

@@ -28,18 +28,22 @@ import os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_1704_07724_b200", "csrc", "gather_variants.inc")
 
-# (id, name, R, S, P, W, TY, KL, NW, CH, STAGES): stride 1 only.  W = input width.
+# (id, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES): stride 1 only.  W = input width.
+# NW warps per CTA, MINB CTAs per SM (register budget 65536 / (32*NW*MINB)).
 VARIANTS = [
-    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 8, 8, 4),      # C2, C5 (AlexNet conv3/4/5)
-    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 8, 8, 4),      # C4a (inception-3a 3x3)
-    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 8, 4, 4),      # C3 (AlexNet conv2, groups 2)
-    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 8, 4, 4),      # C4b (inception-3a 5x5)
-    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 8, 4, 4),      # C1 (LeNet conv2)
-    (6, "r3s3p1_w13_ty13_kl1", 3, 3, 1, 13, 13, 1, 8, 16, 4),   # C2 alternative (whole plane, 32 k/warp)
+    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 8, 1, 8, 4),      # C2, C5 (AlexNet conv3/4/5)
+    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 8, 1, 8, 4),      # C4a (inception-3a 3x3)
+    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 8, 1, 4, 4),      # C3 (AlexNet conv2, groups 2)
+    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 8, 1, 4, 4),      # C4b (inception-3a 5x5)
+    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 8, 1, 4, 4),      # C1 (LeNet conv2)
+    (6, "r3s3p1_w13_ty13_kl1", 3, 3, 1, 13, 13, 1, 8, 1, 16, 4),   # C2 alternative (whole plane, 32 k/warp)
+    (7, "r3s3p1_w13_ty7_kl1_nw12", 3, 3, 1, 13, 7, 1, 12, 1, 16, 4),  # C2: 3 warps/SMSP
+    (8, "r3s3p1_w13_ty4_kl2_nw12", 3, 3, 1, 13, 4, 2, 12, 1, 8, 4),   # C2: 3 warps/SMSP
+    (9, "r3s3p1_w13_ty7_kl1_nw8x2", 3, 3, 1, 13, 7, 1, 8, 2, 8, 3),   # C2: 2 CTAs/SM
 ]
 
 
-def gen_variant(vid, name, R, S, P, W, TY, KL, NW, CH, STAGES):
+def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
     WO = W + 2 * P - S + 1
     NX = WO if KL == 2 else (WO + 1) // 2          # accumulator columns per row
     NWR = TY + R - 1                                 # window rows
@@ -94,12 +98,15 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, CH, STAGES):
             n_fma += len(body)
     # ---- threaded interpreter over a shared-memory entry stream ----------
     # entry = (x, code): code < NCASES: nonzero with value bits x at window
-    # position `code`; code == NCASES: load the lane's weights of the channel
-    # whose byte offset in the weight stage is x; code == NCASES+1: exit.
+    # position `code`; code == NCASES: channel marker, x = channel index ->
+    # load the lane's weights of channel x from the weight stage;
+    # code == NCASES+1: exit.
     # The next entry is loaded before the current one is dispatched.
     LW, EXIT = NCASES, NCASES + 1
-    pop = vop   # %pop: stream pointer (u32 smem address); %wop_base: lane weight base
-    wlop = vop + 1
+    pop = vop   # %pop: stream pointer (u32 smem address)
+    wlop = vop + 1   # lane's weight address of the chunk's first channel
+    cbop = vop + 2   # global index of the chunk's first channel
+    chb = R * S * 32 * KL * 4   # bytes of one channel in the weight stage
     asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea;", ".reg .f32 al, ah, wl, wh, vf;",
            f"mov.b32 ep, %{pop};",
            "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
@@ -116,7 +123,8 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, CH, STAGES):
             asm += [x.replace(f"%{vop},", "vf,") for x in b]
             asm.append("bra.uni LOOP_%=;")
     asm.append("LW_%=:")
-    asm.append(f"add.u32 ea, %{wlop}, xc;")
+    asm.append(f"sub.u32 ea, xc, %{cbop};")
+    asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
     if KL == 2:
         for i in range(len(wops)):
             asm.append(f"ld.shared.b64 %{wop[wops[i]]}, [ea+{i * 256}];")
@@ -133,21 +141,22 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, CH, STAGES):
              f"{n_fma} FMA instructions over {NCASES} window positions"]
     lines.append(f"struct V{vid} {{")
     for k, v in (("R", R), ("S", S), ("P", P), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
-                 ("NW", NW), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
+                 ("NW", NW), ("MINB", MINB), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
                  ("NWOPS", len(wops))):
         lines.append(f"    static constexpr int {k} = {v};")
     lines.append(f'    static constexpr const char* NAME = "{name}";')
     lines.append(f"    static constexpr int LOADW = {LW}, EXIT = {EXIT};")
     lines.append("    // Run the entry stream at shared address `stream` (see tools/gen_gather.py).")
     lines.append("    // acc[ty][m], wp[i]: f32x2 bit patterns (x in the low word); wlane: shared")
-    lines.append("    // address of this lane's weights of channel 0 of the current stage.")
+    lines.append("    // address of this lane's weights of channel `cbase` (first channel of the stage).")
     lines.append("    __device__ __forceinline__ static void run(unsigned long long (&acc)[TY][NX], "
-                 "unsigned long long (&wp)[NWOPS], const unsigned stream, const unsigned wlane) {")
+                 "unsigned long long (&wp)[NWOPS], const unsigned stream, const unsigned wlane, "
+                 "const unsigned cbase) {")
     lines.append("        asm volatile(")
     for a in asm:
         lines.append(f'            "{a}\\n\\t"')
     outs = ", ".join([f'"+l"(acc[{ty}][{m}])' for (ty, m) in accs] + [f'"+l"(wp[{i}])' for i in range(len(wops))])
-    ins = '"r"(stream), "r"(wlane)'
+    ins = '"r"(stream), "r"(wlane), "r"(cbase)'
     lines.append(f"            : {outs}")
     lines.append(f"            : {ins}")
     lines.append('            : "memory");')
