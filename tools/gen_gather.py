@@ -42,6 +42,9 @@ VARIANTS = [
     (9, "r3s3p1_w13_ty7_kl1_nw8x2", 3, 3, 1, 13, 7, 1, 8, 2, 8, 3),   # C2: 2 CTAs/SM
 ]
 
+# C2 s=0.95 gather (B200, round 1): V7 232 us, V1 331 us, V8 340 us, V6 393 us, V9 422 us
+PRIORITY = [7, 1, 8, 6, 9]
+
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
     WO = W + 2 * P - S + 1
@@ -171,8 +174,10 @@ def main():
     for v in VARIANTS:
         parts.append(gen_variant(*v))
         parts.append("")
+    # selection order = first match wins: measured fastest first
+    order = sorted(VARIANTS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
     parts.append("#define SC_GATHER_VARIANTS(X) \\")
-    parts.append(" \\\n".join(f"    X(V{v[0]})" for v in VARIANTS))
+    parts.append(" \\\n".join(f"    X(V{v[0]})" for v in order))
     parts.append("")
     with open(OUT, "w") as f:
         f.write("\n".join(parts))
