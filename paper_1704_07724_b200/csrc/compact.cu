@@ -9,148 +9,182 @@
 // ascending; offs[n][t][c] = index of channel c's marker, offs[..][C] = length.
 // The stream is exactly the instruction stream the stage-2 interpreter runs.
 //
-// Design: one CTA of 8 warps per stream.
-//  pass 1: warp w counts the nonzeros of channels w, w+8, ... inside the
-//          window (a contiguous run of the flat NCHW array, generally not
-//          16-byte aligned: 16-byte-aligned LDG.128 over the covering float4s,
-//          masked head/tail, __ballot_sync + __popc);
-//  scan:   warp 0 turns the per-channel sizes (1 + count) into offsets
-//          (shuffle scan), written to global;
-//  pass 2: the same warps re-read their channels (L1/L2 hits) and write the
-//          marker and the entries at their ranks.
-// HBM traffic: the input once (+ the halo rows shared by neighbouring tiles)
-// and 8 bytes per written entry.
+// Design: one CTA per stream, one pass over the data.
+// The window rows of one channel are a single contiguous run of the NCHW
+// array (`seg` floats).  Channels are processed in rounds of NW*RCH (warp w
+// owns channels w, w+NW, ...).  In a round every lane issues all its loads
+// at once (RCH channels x KV coalesced 4-byte loads, lanes over the run), so
+// one HBM/L2 round trip covers the round; __ballot_sync masks of the loaded
+// values give the per-channel counts, a block scan of (1 + count) gives every
+// channel's marker index (-> offs), and the same masks place each nonzero at
+// its rank (__popc of the lower lanes) -- values are written from registers,
+// nothing is re-read.  Runs longer than 32*KV floats are handled in blocks
+// (counted first, re-loaded for the emit).
 #include "sc_internal.h"
 
 namespace sc {
 
 namespace {
-
-__device__ __forceinline__ float4 ld_f4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-
-// The covering float4 of element e0 (multiple of 4), zero outside [lo, hi)
-// and beyond the tensor end.
-__device__ __forceinline__ float4 load_chunk(const float* __restrict__ in, int64_t e0, int64_t hi, int64_t total) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 < hi) {
-        if (e0 + 3 < total) {
-            v = ld_f4(in + e0);
-        } else {
-            v.x = in[e0];
-            if (e0 + 1 < total) v.y = in[e0 + 1];
-            if (e0 + 2 < total) v.z = in[e0 + 2];
-        }
-    }
-    return v;
-}
-
-__device__ __forceinline__ unsigned nz_mask(float4 v, int64_t e0, int64_t lo, int64_t hi) {
-    const float q[4] = {v.x, v.y, v.z, v.w};
-    unsigned m = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (e0 + j >= lo && e0 + j < hi && q[j] != 0.0f) m |= 1u << j;  // IEEE: -0.0 is zero
-    return m;
-}
-
+constexpr int kRegs = 16;  // RCH * KV: values held per lane per round
 }  // namespace
 
-__global__ void __launch_bounds__(256) compact_streams_kernel(const float* __restrict__ in, int C, int H, int W,
-                                                              int TY, int tiles, int T, int P, int NWR, int NWIN,
-                                                              int64_t cap, int64_t total,
-                                                              uint2* __restrict__ entries,
-                                                              uint32_t* __restrict__ offs) {
-    extern __shared__ uint32_t cnt_s[];  // [C + 1]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int KV>
+__global__ void __launch_bounds__(512) compact_streams_kernel(const float* __restrict__ in, int C, int H, int W,
+                                                               int TY, int tiles, int T, int P, int NWR, int NWIN,
+                                                               int64_t cap, uint2* __restrict__ entries,
+                                                               uint32_t* __restrict__ offs) {
+    constexpr int RCH = kRegs / KV;  // channels per warp per round
+    constexpr int BLK = 32 * KV;     // floats per load block
+    __shared__ uint32_t start_s[32 * RCH];
+    __shared__ uint32_t wsum_s[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int stream = blockIdx.x;
     const int n = stream / tiles, t = stream - n * tiles;
     const int i_lo = t * TY * T - P;
     const int r0 = i_lo < 0 ? 0 : i_lo;
     const int r1 = (i_lo + NWR < H) ? i_lo + NWR : H;
-    const int64_t seg = r1 > r0 ? (int64_t)(r1 - r0) * W : 0;
+    const int seg = r1 > r0 ? (r1 - r0) * W : 0;        // window rows: one contiguous run per plane
+    const unsigned shift = (unsigned)((r0 - i_lo) * W);  // window position of the run's first element
     const unsigned lt = (1u << lane) - 1u;
+    const float* img = in + (int64_t)n * C * H * W + (int64_t)r0 * W;
+    uint2* st = entries + (int64_t)stream * cap;
+    uint32_t* of = offs + (int64_t)stream * (C + 1);
+    const int per_round = nw * RCH;
 
-    // ---- pass 1: per-channel window counts
-    for (int c = warp; c < C; c += 8) {
-        const int64_t plane = ((int64_t)n * C + c) * H * W;
-        const int64_t lo = plane + (int64_t)r0 * W, hi = lo + seg;
-        unsigned cnt = 0;
-        for (int64_t b = lo & ~(int64_t)3; b < hi; b += 256) {  // two float4 per lane in flight
-            const float4 v0 = load_chunk(in, b + 4 * lane, hi, total);
-            const float4 v1 = load_chunk(in, b + 128 + 4 * lane, hi, total);
-            cnt += __popc(nz_mask(v0, b + 4 * lane, lo, hi)) + __popc(nz_mask(v1, b + 128 + 4 * lane, lo, hi));
-        }
+    uint32_t base = 0;
+    for (int cb = 0; cb < C; cb += per_round) {
+        const int nround = (C - cb) < per_round ? (C - cb) : per_round;
+        // ---- loads of the first block of every owned channel, all in flight
+        float v[RCH][KV];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) cnt_s[c] = cnt;
-    }
-    __syncthreads();
-    // ---- exclusive scan of (1 + count): marker + entries per channel
-    if (warp == 0) {
-        uint32_t running = 0;
-        for (int base = 0; base < C; base += 32) {
-            const int c = base + lane;
-            const uint32_t v = c < C ? 1u + cnt_s[c] : 0u;
-            uint32_t incl = v;
+        for (int q = 0; q < RCH; ++q) {
+            const int ch = warp + q * nw;
+            const float* src = img + (int64_t)(cb + ch) * H * W;
+#pragma unroll
+            for (int u = 0; u < KV; ++u) {
+                const int off = 32 * u + lane;
+                v[q][u] = (ch < nround && off < seg) ? __ldg(src + off) : 0.0f;
+            }
+        }
+        // ---- counts (ballot masks of the first block are kept for the emit)
+        unsigned bal[RCH][KV];
+#pragma unroll
+        for (int q = 0; q < RCH; ++q) {
+            const int ch = warp + q * nw;
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int u = 0; u < KV; ++u) {
+                bal[q][u] = __ballot_sync(0xffffffffu, v[q][u] != 0.0f);  // IEEE: -0.0 is zero
+                cnt += __popc(bal[q][u]);
+            }
+            if (seg > BLK && ch < nround) {  // long runs: count the remaining blocks
+                const float* src = img + (int64_t)(cb + ch) * H * W;
+                for (int o0 = BLK; o0 < seg; o0 += 32) {
+                    const float x = o0 + lane < seg ? __ldg(src + o0 + lane) : 0.0f;
+                    cnt += __popc(__ballot_sync(0xffffffffu, x != 0.0f));
+                }
+            }
+            if (lane == 0 && ch < nround) start_s[ch] = 1u + cnt;
+        }
+        __syncthreads();
+        // ---- block-wide exclusive scan of (1 + count) over the round's channels;
+        // thread i owns channels RCH*i .. RCH*i + RCH-1 of the round
+        {
+            uint32_t a[RCH];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < RCH; ++q) {
+                const int i = RCH * (int)threadIdx.x + q;
+                a[q] = i < nround ? start_s[i] : 0u;
+                mine += a[q];
+            }
+            uint32_t incl = mine;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += u;
             }
-            if (c < C) cnt_s[c] = running + incl - v;
-            running += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) cnt_s[C] = running;
-    }
-    __syncthreads();
-    uint32_t* of = offs + (int64_t)stream * (C + 1);
-    for (int c = threadIdx.x; c <= C; c += blockDim.x) of[c] = cnt_s[c];
-    // ---- pass 2: marker + entries
-    uint2* st = entries + (int64_t)stream * cap;
-    for (int c = warp; c < C; c += 8) {
-        const int64_t plane = ((int64_t)n * C + c) * H * W;
-        const int64_t lo = plane + (int64_t)r0 * W, hi = lo + seg;
-        const int64_t code0 = plane + (int64_t)i_lo * W;  // code = e - code0 = (i - i_lo)*W + j
-        uint32_t pos = cnt_s[c];
-        if (lane == 0) st[pos] = make_uint2((unsigned)c, (unsigned)NWIN);
-        ++pos;
-        for (int64_t b = lo & ~(int64_t)3; b < hi; b += 128) {
-            const int64_t e0 = b + 4 * lane;
-            const float4 v = load_chunk(in, e0, hi, total);
-            const unsigned m = nz_mask(v, e0, lo, hi);
-            const float q[4] = {v.x, v.y, v.z, v.w};
-            unsigned before = 0, tot = 0;
+            if (lane == 31) wsum_s[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t x = lane < nw ? wsum_s[lane] : 0u;
+                uint32_t xi = x;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned bal = __ballot_sync(0xffffffffu, (m >> j) & 1u);
-                before += __popc(bal & lt);
-                tot += __popc(bal);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
+                    if (lane >= o) xi += u;
+                }
+                wsum_s[lane] = xi - x;  // exclusive warp offsets
+                if (lane == 31) wsum_s[32] = xi;  // round total
             }
-            uint32_t p = pos + before;
+            __syncthreads();
+            uint32_t excl = base + wsum_s[warp] + incl - mine;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((m >> j) & 1u) {
-                    st[p] = make_uint2(__float_as_uint(q[j]), (unsigned)(e0 + j - code0));
-                    ++p;
+            for (int q = 0; q < RCH; ++q) {
+                const int i = RCH * (int)threadIdx.x + q;
+                if (i < nround) {
+                    start_s[i] = excl;
+                    of[cb + i] = excl;
+                }
+                excl += a[q];
+            }
+            __syncthreads();
+        }
+        // ---- emit: marker + entries at their ranks (first block from registers)
+#pragma unroll
+        for (int q = 0; q < RCH; ++q) {
+            const int ch = warp + q * nw;
+            if (ch < nround) {
+                uint32_t pos = start_s[ch];
+                if (lane == 0) st[pos] = make_uint2((unsigned)(cb + ch), (unsigned)NWIN);
+                ++pos;
+#pragma unroll
+                for (int u = 0; u < KV; ++u) {
+                    if (v[q][u] != 0.0f)
+                        st[pos + __popc(bal[q][u] & lt)] =
+                            make_uint2(__float_as_uint(v[q][u]), shift + (unsigned)(32 * u + lane));
+                    pos += __popc(bal[q][u]);
+                }
+                if (seg > BLK) {
+                    const float* src = img + (int64_t)(cb + ch) * H * W;
+                    for (int o0 = BLK; o0 < seg; o0 += 32) {
+                        const float x = o0 + lane < seg ? __ldg(src + o0 + lane) : 0.0f;
+                        const unsigned b = __ballot_sync(0xffffffffu, x != 0.0f);
+                        if (x != 0.0f)
+                            st[pos + __popc(b & lt)] = make_uint2(__float_as_uint(x), shift + (unsigned)(o0 + lane));
+                        pos += __popc(b);
+                    }
                 }
             }
-            pos += tot;
         }
+        base += wsum_s[32];
+        __syncthreads();  // start_s / wsum_s are reused by the next round
     }
+    if (threadIdx.x == 0) of[C] = base;
 }
 
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint2* entries, uint32_t* offs,
                            cudaStream_t st) {
-    const int64_t streams = n * g.tiles;
-    const size_t smem = sizeof(uint32_t) * (g.C + 1);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(compact_streams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    compact_streams_kernel<<<(unsigned)streams, 256, smem, st>>>(
-        in, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.tiles, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-        g.cap, n * g.C * g.H * g.W, entries, offs);
+    const int64_t rows = g.nwr < g.H ? g.nwr : g.H;
+    const int64_t seg = rows * g.W;
+    const int kv = seg <= 32 ? 1 : seg <= 64 ? 2 : seg <= 128 ? 4 : 8;
+    const int rch = kRegs / kv;
+    // enough warps for every channel in one round, at most 16 (several CTAs per SM overlap
+    // one CTA's scan with another's loads)
+    int64_t warps = (g.C + rch - 1) / rch;
+    if (warps > 16) warps = 16;
+    if (warps < 2) warps = 2;
+    const unsigned threads = (unsigned)(32 * warps);
+    const unsigned grid = (unsigned)(n * g.tiles);
+#define SC_LAUNCH_KV(K)                                                                                            \
+    compact_streams_kernel<K><<<grid, threads, 0, st>>>(in, (int)g.C, (int)g.H, (int)g.W, (int)g.ty,               \
+                                                        (int)g.tiles, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, \
+                                                        g.cap, entries, offs)
+    if (kv == 1) SC_LAUNCH_KV(1);
+    else if (kv == 2) SC_LAUNCH_KV(2);
+    else if (kv == 4) SC_LAUNCH_KV(4);
+    else SC_LAUNCH_KV(8);
+#undef SC_LAUNCH_KV
     return cudaGetLastError();
 }
 

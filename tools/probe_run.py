@@ -1,8 +1,9 @@
-"""Quick GPU probe: FMA-pipe rates and per-stage timings of the sparse path on
-C2 (AlexNet conv3, N=128).  Prints plain text; not a bench line."""
+"""Quick GPU probe: FMA-pipe rates and per-stage device times of the sparse
+path (and the dense path) per config.  Device times come from CUDA graphs that
+hold `reps` back-to-back launches (host launch cost excluded).  Plain text; not
+a bench line.  Usage: python tools/probe_run.py [cfg ...]"""
 import os
 import sys
-import time
 
 import torch
 
@@ -10,39 +11,46 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1704_07724_b200 import datagen, sparseconv as sc  # noqa: E402
 
 
-def timeit(fn, reps=20, warm=3):
-    for _ in range(warm):
+def dev_time_us(fn, reps=20):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
         fn()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        s.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
+        a.record(s)
+        g.replay()
+        b.record(s)
         b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
-    ts.sort()
-    return ts[len(ts) // 2]
+    return a.elapsed_time(b) * 1e3 / reps
 
 
 def main():
-    for kind, name in ((0, "FFMA"), (1, "FFMA2"), (2, "FFMA2+int")):
+    cfgs = sys.argv[1:] or ["C2", "C4a", "C3", "C1", "C4b"]
+    for kind, name in ((0, "FFMA"), (1, "FFMA2")):
         print(f"probe {name}: {sc.probe_fma(kind):.1f} lane-FMA/clk/SM")
-    for cfg in ("C2", "C4a", "C3", "C1", "C4b"):
-        for s in (0.9, 0.95, 0.99) if cfg != "C3" else ("channel",):
+    for cfg in cfgs:
+        for s in datagen.CONFIG_SPARSITY[cfg]:
             shp = datagen.CONFIGS[cfg]
             x = torch.from_numpy(datagen.activations(shp, s)).cuda()
             w, b = datagen.weights(shp)
             conv = sc.SparseConv(torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), shp.n, shp.c, shp.h,
                                  shp.w, shp.stride, shp.pad, shp.groups)
             out = conv.forward(x)
-            t_c = timeit(lambda: conv.compact(x))
-            t_g = timeit(lambda: conv.gather(shp.n, out))
-            t_f = timeit(lambda: conv.forward(x, out))
-            print(f"{cfg} s={s} variant={conv.variant} compact={t_c:.1f}us gather={t_g:.1f}us forward={t_f:.1f}us")
-            if cfg in ("C1", "C4b"):
-                break
+            t_c = dev_time_us(lambda: conv.compact(x))
+            t_g = dev_time_us(lambda: conv.gather(shp.n, out))
+            t_f = dev_time_us(lambda: conv.forward(x, out))
+            try:
+                t_d = dev_time_us(lambda: conv.dense_forward(x, out))
+            except sc.SparseConvError:
+                t_d = float("nan")
+            print(f"{cfg} s={s} variant={conv.variant} compact={t_c:.1f}us gather={t_g:.1f}us "
+                  f"forward={t_f:.1f}us dense_tc={t_d:.1f}us")
 
 
 if __name__ == "__main__":
