@@ -10,7 +10,9 @@
 //    channels).  The packed weight slice wpack[g][kb][c0:c0+CH][R][S][KBW] of
 //    CH input channels is ONE contiguous run, streamed through a STAGES-deep
 //    shared-memory ring by 1-D TMA bulk copies (cp.async.bulk + mbarrier
-//    complete_tx); thread 0 refills a stage once all active warps released it.
+//    complete_tx) issued by a dedicated producer warp (warp NW), which refills
+//    a stage once all active compute warps released it (no compute warp ever
+//    waits for another except through the ring depth).
 //  * warp = one unit = one stage-1 tile stream (image n, output rows
 //    [y0, y0+TY)); lane owns KL output channels (the paper's "4 floats of
 //    weights ... at one time", becomes 32*KL per warp).  The warp's
@@ -100,7 +102,7 @@ struct Smem {
 };
 
 template <class V>
-__global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const Args a) {
+__global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(const Args a) {
     using SM = Smem<V>;
     constexpr int RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO;
     constexpr int CH = V::CH, STAGES = V::STAGES, NW = V::NW, KBW = SM::KBW;
@@ -130,15 +132,20 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < STAGES && q < nchunks; ++q) {
-            const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
-            const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
-            mbar_expect_tx(&full[q], bytes);
-            tma_bulk_g2s(ring + q * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[q]);
+    if (warp == NW) {  // producer warp: streams the weight chunks through the ring
+        if (lane == 0) {
+            for (int q = 0; q < nchunks; ++q) {
+                const int qs = q % STAGES;
+                if (q >= STAGES) mbar_wait(&empty[qs], ((q / STAGES) - 1) & 1);  // all warps released it
+                const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
+                const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
+                mbar_expect_tx(&full[qs], bytes);
+                tma_bulk_g2s(ring + qs * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[qs]);
+            }
         }
+        return;
     }
-    if (!active) return;  // warp 0 is always active (every CTA has >= 1 unit)
+    if (!active) return;
 
     const int n = unit / a.ytiles;
     const int y0 = (unit % a.ytiles) * TY;
@@ -148,14 +155,24 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
     uint64_t* pbar = pbar_all + warp * kSlots;
     uint2* pieces = piece_all + warp * kSlots * (kPiece + 2);
 
-    unsigned long long acc[TY][NX];  // f32x2 bit patterns, low word = first element
+    // f32x2 bit patterns (low word = first element): channel pairs (KL >= 2) or
+    // x pairs (KL == 1); odd KL adds one f32 accumulator per pixel
+    unsigned long long accp[TY][NX][V::NPAIR];
+    float accs[TY][NX];
 #pragma unroll
     for (int ty = 0; ty < TY; ++ty)
 #pragma unroll
-        for (int m = 0; m < NX; ++m) acc[ty][m] = 0ull;
-    unsigned long long wp[V::NWOPS];
+        for (int m = 0; m < NX; ++m) {
 #pragma unroll
-    for (int i = 0; i < V::NWOPS; ++i) wp[i] = 0ull;
+            for (int pi = 0; pi < V::NPAIR; ++pi) accp[ty][m][pi] = 0ull;
+            accs[ty][m] = 0.0f;
+        }
+    unsigned long long wp[V::NWP];
+    float ws[V::NWS];
+#pragma unroll
+    for (int i = 0; i < V::NWP; ++i) wp[i] = 0ull;
+#pragma unroll
+    for (int i = 0; i < V::NWS; ++i) ws[i] = 0.0f;
 
     // Chunk boundaries bnd(q) = of[min(q*CH, Cg)], q <= nchunks (<= 63), held
     // two per lane and broadcast with shuffles.
@@ -200,7 +217,11 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
     for (int ch = 0; ch < nchunks; ++ch) {
         const int st = ch % STAGES;
         const uint32_t chunk_end = bnd(ch + 1);
-        const unsigned wlane = smem_u32(ring + st * SM::kStageFloats) + lane * 4 * V::KL;
+        const unsigned wstage = smem_u32(ring + st * SM::kStageFloats);
+        // lane's weights in a tap block of 32*KL floats (pack.cu): KL=1,2,4 lane-contiguous
+        // runs of KL floats; KL=3 a pair at 8*lane and a single at 256 + 4*lane
+        const unsigned wlane = wstage + lane * (V::XPAIR ? 4u : 8u * V::NPAIR);
+        const unsigned wlane_s = wstage + lane * 4u;
         const unsigned cbase = (unsigned)(g * a.Cg + ch * CH);
         mbar_wait(&full[st], (ch / STAGES) & 1);  // this chunk's weights have landed
 #pragma unroll 1
@@ -211,7 +232,7 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
             uint2* p = pieces + slot * (kPiece + 2) + (ca & 1u);
             if (lane == 0) p[b - ca] = make_uint2(0u, (unsigned)V::EXIT);
             __syncwarp();
-            V::run(acc, wp, smem_u32(p), wlane, cbase);
+            V::run(accp, accs, wp, ws, smem_u32(p), wlane, wlane_s, cbase);
             __syncwarp();
             ++consumed;
             ca = b;
@@ -219,44 +240,21 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
-        if (threadIdx.x == 0 && ch >= 1) {
-            const int q = ch - 1 + STAGES;
-            if (q < nchunks) {
-                const int qs = (ch - 1) % STAGES;
-                mbar_wait(&empty[qs], ((ch - 1) / STAGES) & 1);
-                const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
-                const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
-                mbar_expect_tx(&full[qs], bytes);
-                tma_bulk_g2s(ring + qs * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[qs]);
-            }
-        }
     }
 
-    // Epilogue: registers -> smem [k][rows*WO] -> contiguous NCHW runs.
+    // Epilogue: registers -> smem [k][rows*WO] -> contiguous NCHW runs, + bias,
+    // optional ReLU (Eq. 2).  One pass per channel slot h of a lane (KL >= 2:
+    // channel kloc + KL*lane + h; KL == 1: channel kloc + lane, pixels in pairs).
     constexpr int ER = SM::kER, ES = SM::kEpiStride;
     float* epi = reinterpret_cast<float*>(pieces);  // this warp's slots are idle now
     const int kloc = kb * KBW;
-    // bias (+ ReLU, Eq. 2) in registers: lane owns channels kloc + KL*lane + {0, KL-1} (KL=2)
-    // or kloc + lane (KL=1)
-    {
-        const int k0 = kloc + V::KL * lane;
-        const float b0 = k0 < a.Kg ? __ldg(&a.bias[g * a.Kg + k0]) : 0.f;
-        const float b1 = (V::KL == 2 && k0 + 1 < a.Kg) ? __ldg(&a.bias[g * a.Kg + k0 + 1]) : b0;
-#pragma unroll
-        for (int ty = 0; ty < TY; ++ty)
-#pragma unroll
-            for (int m = 0; m < NX; ++m) {
-                float lo = __uint_as_float((unsigned)acc[ty][m]) + b0;
-                float hi = __uint_as_float((unsigned)(acc[ty][m] >> 32)) + b1;
-                if (a.relu) {
-                    lo = fmaxf(lo, 0.f);
-                    hi = fmaxf(hi, 0.f);
-                }
-                acc[ty][m] = (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
-            }
-    }
     const int krows = (a.Kg - kloc) < KBW ? (a.Kg - kloc) : KBW;  // valid output channels of this block
-    // KL=2: one pass per pair half (h=0: k = 2*lane, h=1: k = 2*lane+1)
+    float bv[V::KL];
+#pragma unroll
+    for (int h = 0; h < V::KL; ++h) {
+        const int k = kloc + V::KL * lane + h;
+        bv[h] = k < a.Kg ? __ldg(&a.bias[g * a.Kg + k]) : 0.0f;
+    }
 #pragma unroll
     for (int h = 0; h < V::KL; ++h)
 #pragma unroll
@@ -266,13 +264,27 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
             if (r0 + rr < TY) {
 #pragma unroll
                 for (int m = 0; m < NX; ++m) {
-                    const float lo = __uint_as_float((unsigned)acc[r0 + rr][m]);
-                    const float hi = __uint_as_float((unsigned)(acc[r0 + rr][m] >> 32));
-                    if constexpr (V::KL == 2) {  // channel 2*lane+h of pixel x = m
-                        epi[lane * ES + rr * WO + m] = h ? hi : lo;
-                    } else {                     // (x = 2m, 2m+1) of channel k = lane
+                    if constexpr (V::XPAIR) {  // (x = 2m, 2m+1) of channel k = lane
+                        const unsigned long long u = accp[r0 + rr][m][0];
+                        float lo = __uint_as_float((unsigned)u) + bv[0];
+                        float hi = __uint_as_float((unsigned)(u >> 32)) + bv[0];
+                        if (a.relu) {
+                            lo = fmaxf(lo, 0.f);
+                            hi = fmaxf(hi, 0.f);
+                        }
                         epi[lane * ES + rr * WO + 2 * m] = lo;
                         if (2 * m + 1 < WO) epi[lane * ES + rr * WO + 2 * m + 1] = hi;
+                    } else {  // channel slot h of pixel x = m
+                        float o;
+                        if (h < 2 * V::NPAIR) {
+                            const unsigned long long u = accp[r0 + rr][m][h / 2];
+                            o = __uint_as_float((h & 1) ? (unsigned)(u >> 32) : (unsigned)u);
+                        } else {
+                            o = accs[r0 + rr][m];
+                        }
+                        o += bv[h];
+                        if (a.relu) o = fmaxf(o, 0.f);
+                        epi[lane * ES + rr * WO + m] = o;
                     }
                 }
             }
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(V::NW * 32, V::MINB) gather_fast_kernel(const 
         if (rows > 0) {
             // flattened (channel row kk, pixel p) loop: 32 consecutive elements per step
             const int len = rows * WO;
-            const int nrows = V::KL == 2 ? (krows - h + 1) / 2 : krows;
+            const int nrows = (krows - h + V::KL - 1) / V::KL;  // lanes whose slot h is a valid channel
             const int total = nrows * len;
             float* dst0 = a.out + ((size_t)(n * a.K + g * a.Kg + kloc + h) * a.Ho + y0 + r0) * WO;
             const size_t kstride = (size_t)a.Ho * WO * V::KL;
@@ -315,7 +327,7 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
-    kern<<<(unsigned)grid, V::NW * 32, smem, st>>>(a);
+    kern<<<(unsigned)grid, (V::NW + 1) * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 

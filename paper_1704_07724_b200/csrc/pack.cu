@@ -5,7 +5,7 @@
 // that stores kernels (say 4 floats of weights: W_{k..k+3,c,i-r,j-s}) can be
 // fetched".  On the GPU the contiguous run over k is a warp's 32 lanes:
 //
-//   wpack[g][kb][cl][r][t][j] = W[g*Kg + kbw*kb + j][cl][r][t]
+//   wpack[g][kb][cl][r][t][j] = W[g*Kg + kbw*kb + jj(j)][cl][r][t]   (jj(j) = j for KL != 3)
 //   (zero for kbw*kb + j >= Kg; kb < Kg_pad/kbw; kbw = 32*KL of the stage-2 kernel)
 //
 // so the lanes of a warp read consecutive 4-byte (KL=1) or 8-byte (KL=2)
@@ -31,7 +31,13 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
         const int64_t kblocks = Kg_pad / kbw;
         const int64_t kb = rest % kblocks;
         const int64_t g = rest / kblocks;
-        const int64_t kk = kb * kbw + j;
+        // position j of a tap block -> channel offset within the k-block: lane l owns
+        // channels KL*l .. KL*l+KL-1; KL=1,2,4 store them contiguously, KL=3 stores
+        // the pair (3l, 3l+1) at 2l and the single 3l+2 at 64 + l (8- and 4-byte
+        // shared loads without bank conflicts)
+        int64_t jj = j;
+        if (kbw == 96) jj = j < 64 ? 3 * (j / 2) + (j % 2) : 3 * (j - 64) + 2;
+        const int64_t kk = kb * kbw + jj;
         float v = 0.0f;
         if (kk < Kg) v = w[((g * Kg + kk) * Cg + cl) * RS + rs];
         wpack[o] = v;

@@ -9,17 +9,23 @@ product I_{c,i,j} x W_{k,c,i-r,j-s} for an output O_{k,i+r,j+s}", PAPER.md:121,
 with the inverse index map of reading R6: y = i + P - r, x = j + P - t).  The
 blocks are emitted as inline PTX behind ONE `brx.idx.uni` jump table (SASS:
 LDC + BRX per nonzero); a C++ `switch` is lowered by the NVVM front end to a
-compare tree (~12 branches per nonzero) instead.
+compare tree instead, and a dispatch at the end of every block ("threaded
+code") gets one PC-relative jump table per site (constant-cache thrash,
+measured 2-4x slower).
 
-Two register-tile forms (KL = output channels per lane):
-* KL=2: acc[ty][x] is an f32x2 pair over two adjacent output channels
-  (k0, k0+1) of pixel (y0+ty, x); one FFMA2 (fma.rn.f32x2, nonzero value as a
-  broadcast scalar) per in-tile tap: acc[ty][x] += v * (W[k0][r][t], W[k0+1][r][t]).
-  No lane is wasted; the weight operand is a natural 64-bit shared-memory load.
-* KL=1: acc[ty][m] pairs two horizontally adjacent outputs (x = 2m, 2m+1) of
-  one output channel.  Where both outputs are in the nonzero's footprint one
-  FFMA2 with the weight pair (W[r][u], W[r][u-1]), u = j + P - 2m, updates both;
-  where only one is, a single FFMA updates that half.  No zero-padded weights.
+Register-tile forms (KL = output channels per lane, lane l owns channels
+KL*l .. KL*l+KL-1 of the warp's k-block):
+* KL=1 "x-pair": acc[ty][m] pairs two horizontally adjacent outputs
+  (x = 2m, 2m+1) of one channel.  Where both outputs are in the nonzero's
+  footprint one FFMA2 with the weight pair (W[r][u], W[r][u-1]), u = j+P-2m,
+  updates both; where only one is, a single FFMA.
+* KL>=2: per output pixel NPAIR = KL/2 f32x2 accumulators over channel pairs
+  (k0,k1), (k2,k3) and, for odd KL, one f32 accumulator (k2).  Per in-tile tap:
+  NPAIR FFMA2 (nonzero value as broadcast scalar) + one FFMA for odd KL.
+  The weights of a tap are one 64-bit (KL=2), one 128-bit (KL=4) or a 64-bit
+  + 32-bit pair of shared-memory loads (KL=3, layout of pack.cu).
+Every FMA issue slot retires KL lane-FMAs per in-tile tap: the work per
+(~8-instruction, ~100-cycle-latency) dispatch grows with KL.
 
 Usage: python tools/gen_gather.py  (rewrites the .inc; commit the result).
 """
@@ -29,43 +35,70 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_1704_07724_b200", "csrc", "gather_variants.inc")
 
 # (id, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES): stride 1 only.  W = input width.
-# NW warps per CTA, MINB CTAs per SM (register budget 65536 / (32*NW*MINB)).
+# NW compute warps (+1 producer warp) per CTA, MINB CTAs per SM (register budget
+# 65536 / (32*(NW+1)*MINB)).
 VARIANTS = [
-    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 8, 1, 8, 4),      # C2, C5 (AlexNet conv3/4/5)
-    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 8, 1, 8, 4),      # C4a (inception-3a 3x3)
-    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 8, 1, 4, 4),      # C3 (AlexNet conv2, groups 2)
-    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 8, 1, 4, 4),      # C4b (inception-3a 5x5)
-    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 8, 1, 4, 4),      # C1 (LeNet conv2)
-    (6, "r3s3p1_w13_ty13_kl1", 3, 3, 1, 13, 13, 1, 8, 1, 16, 4),   # C2 alternative (whole plane, 32 k/warp)
-    (7, "r3s3p1_w13_ty7_kl1_nw12", 3, 3, 1, 13, 7, 1, 12, 1, 16, 4),  # C2: 3 warps/SMSP
-    (8, "r3s3p1_w13_ty4_kl2_nw12", 3, 3, 1, 13, 4, 2, 12, 1, 8, 4),   # C2: 3 warps/SMSP
-    (9, "r3s3p1_w13_ty7_kl1_nw8x2", 3, 3, 1, 13, 7, 1, 8, 2, 8, 3),   # C2: 2 CTAs/SM
+    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 7, 1, 8, 4),      # C2, C5 (AlexNet conv3/4/5)
+    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 7, 1, 8, 4),      # C4a (inception-3a 3x3)
+    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 7, 1, 4, 4),      # C3 (AlexNet conv2, groups 2)
+    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 7, 1, 4, 4),      # C4b (inception-3a 5x5)
+    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 (LeNet conv2)
+    (7, "r3s3p1_w13_ty7_kl1_nw11", 3, 3, 1, 13, 7, 1, 11, 1, 16, 4),  # C2: x-pairs, 3 warps/SMSP
+    (10, "r3s3p1_w13_ty3_kl3_nw11", 3, 3, 1, 13, 3, 3, 11, 1, 8, 4),  # C2: k-triples, 3 warps/SMSP
+    (11, "r3s3p1_w13_ty3_kl4_nw7", 3, 3, 1, 13, 3, 4, 7, 1, 8, 3),    # C2: k-quads, 2 warps/SMSP
+    (12, "r3s3p1_w13_ty2_kl4_nw11", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3),  # C2: k-quads, 3 warps/SMSP
+    (13, "r3s3p1_w13_ty5_kl2_nw11", 3, 3, 1, 13, 5, 2, 11, 1, 8, 4),  # C2: k-pairs, 3 warps/SMSP
+    (14, "r3s3p1_w28_ty1_kl4_nw11", 3, 3, 1, 28, 1, 4, 11, 1, 8, 3),  # C4a: k-quads
 ]
 
-# C2 s=0.95 gather (B200, round 1): V7 232 us, V1 331 us, V8 340 us, V6 393 us, V9 422 us
-PRIORITY = [7, 1, 8, 6, 9]
+# selection order = first match wins (measured fastest first)
+PRIORITY = [10, 12, 11, 13, 7, 1, 14, 2]
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
     WO = W + 2 * P - S + 1
-    NX = WO if KL == 2 else (WO + 1) // 2          # accumulator columns per row
+    XPAIR = KL == 1
+    NX = (WO + 1) // 2 if XPAIR else WO            # accumulator columns per row
+    NPAIR = 1 if XPAIR else KL // 2                 # f32x2 accumulators per (ty, m)
+    NSING = 0 if XPAIR else KL % 2                  # f32 accumulators per (ty, m)
     NWR = TY + R - 1                                 # window rows
     NCASES = NWR * W
-    accs = [(ty, m) for ty in range(TY) for m in range(NX)]
-    aop = {a: i for i, a in enumerate(accs)}
-    if KL == 2:
-        wops = [(r, t) for r in range(R) for t in range(S)]            # f32x2 (k0, k1) per tap
-    else:
+    ops = []                                         # asm operand list: (constraint, C++ expression)
+    accp = {}
+    for ty in range(TY):
+        for m in range(NX):
+            for pi in range(NPAIR):
+                accp[(ty, m, pi)] = len(ops)
+                ops.append(('"+l"', f"accp[{ty}][{m}][{pi}]"))
+    accs = {}
+    for ty in range(TY):
+        for m in range(NX):
+            for si in range(NSING):
+                accs[(ty, m)] = len(ops)
+                ops.append(('"+f"', f"accs[{ty}][{m}]"))
+    if XPAIR:
         assert S >= 2
-        wops = [(r, u) for r in range(R) for u in range(1, S)]          # pair (W[r][u], W[r][u-1])
-    wop = {w: len(accs) + i for i, w in enumerate(wops)}
-    vop = len(accs) + len(wops)
+        wkeys = [(r, u) for r in range(R) for u in range(1, S)]       # pair (W[r][u], W[r][u-1])
+    else:
+        wkeys = [(r, t) for r in range(R) for t in range(S)]
+    wp = {}
+    for key in wkeys:
+        for pi in range(NPAIR):
+            wp[(key, pi)] = len(ops)
+            ops.append(('"+l"', f"wp[{len(wp) - 1}]"))
+    ws = {}
+    for key in wkeys:
+        for si in range(NSING):
+            ws[key] = len(ops)
+            ops.append(('"+f"', f"ws[{len(ws) - 1}]"))
+    n_out = len(ops)
+    pop, wlop, wsop, cbop = n_out, n_out + 1, n_out + 2, n_out + 3
 
     def scalar(r, t):
         """(operand, half) holding W[r][t] inside the KL=1 weight pairs."""
         if t >= 1:
-            return wop[(r, t)], "lo"          # lo of (W[r][t], W[r][t-1])
-        return wop[(r, 1)], "hi"              # hi of (W[r][1], W[r][0])
+            return wp[((r, t), 0)], "lo"          # lo of (W[r][t], W[r][t-1])
+        return wp[((r, 1), 0)], "hi"              # hi of (W[r][1], W[r][0])
 
     bodies = []
     n_fma = 0
@@ -76,41 +109,42 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
                 r = wi - ty
                 if not (0 <= r < R):
                     continue
-                if KL == 2:
+                if not XPAIR:
                     for x in range(WO):
                         t = j + P - x
                         if 0 <= t < S:
-                            a = aop[(ty, x)]
-                            body.append(f"fma.rn.f32x2 %{a}, %{wop[(r, t)]}, vv, %{a};")
+                            for pi in range(NPAIR):
+                                a = accp[(ty, x, pi)]
+                                body.append(f"fma.rn.f32x2 %{a}, %{wp[((r, t), pi)]}, vv, %{a};")
+                            if NSING:
+                                a = accs[(ty, x)]
+                                body.append(f"fma.rn.f32 %{a}, %{ws[(r, t)]}, vf, %{a};")
                 else:
                     for m in range(NX):
                         x0, x1 = 2 * m, 2 * m + 1
                         t0, t1 = j + P - x0, j + P - x1
                         in0 = 0 <= t0 < S
                         in1 = 0 <= t1 < S and x1 < WO
-                        a = aop[(ty, m)]
+                        a = accp[(ty, m, 0)]
                         if in0 and in1:
-                            body.append(f"fma.rn.f32x2 %{a}, %{wop[(r, t0)]}, vv, %{a};")
+                            body.append(f"fma.rn.f32x2 %{a}, %{wp[((r, t0), 0)]}, vv, %{a};")
                         elif in0 or in1:
                             t = t0 if in0 else t1
                             half = "l" if in0 else "h"
                             o, wh = scalar(r, t)
                             body.append(f"mov.b64 {{al, ah}}, %{a}; mov.b64 {{wl, wh}}, %{o}; "
-                                        f"fma.rn.f32 a{half}, w{wh[0]}, %{vop}, a{half}; mov.b64 %{a}, {{al, ah}};")
+                                        f"fma.rn.f32 a{half}, w{wh[0]}, vf, a{half}; mov.b64 %{a}, {{al, ah}};")
             bodies.append(body)
             n_fma += len(body)
-    # ---- threaded interpreter over a shared-memory entry stream ----------
+    # ---- interpreter over a shared-memory entry stream ------------------
     # entry = (x, code): code < NCASES: nonzero with value bits x at window
     # position `code`; code == NCASES: channel marker, x = channel index ->
     # load the lane's weights of channel x from the weight stage;
-    # code == NCASES+1: exit.
-    # The next entry is loaded before the current one is dispatched.
+    # code == NCASES+1: exit.  The next entry is loaded before the current one
+    # is dispatched.
     LW, EXIT = NCASES, NCASES + 1
-    pop = vop   # %pop: stream pointer (u32 smem address)
-    wlop = vop + 1   # lane's weight address of the chunk's first channel
-    cbop = vop + 2   # global index of the chunk's first channel
     chb = R * S * 32 * KL * 4   # bytes of one channel in the weight stage
-    asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea;", ".reg .f32 al, ah, wl, wh, vf;",
+    asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
            f"mov.b32 ep, %{pop};",
            "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
            "LOOP_%=:",
@@ -123,20 +157,28 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
     for i, b in enumerate(bodies):
         if b:
             asm.append(f"C{i}_%=:")
-            asm += [x.replace(f"%{vop},", "vf,") for x in b]
+            asm += b
             asm.append("bra.uni LOOP_%=;")
     asm.append("LW_%=:")
     asm.append(f"sub.u32 ea, xc, %{cbop};")
+    if NSING:
+        asm.append(f"mad.lo.u32 es, ea, {chb}, %{wsop};")
     asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
-    if KL == 2:
-        for i in range(len(wops)):
-            asm.append(f"ld.shared.b64 %{wop[wops[i]]}, [ea+{i * 256}];")
-    else:
+    tap_bytes = 32 * KL * 4
+    if XPAIR:
         for r in range(R):
             for u in range(1, S):
                 # pair (W[r][u], W[r][u-1]); weights of tap (r,t) at byte (r*S+t)*128 + lane*4
                 asm.append(f"ld.shared.f32 wl, [ea+{(r * S + u) * 128}]; ld.shared.f32 wh, [ea+{(r * S + u - 1) * 128}]; "
-                           f"mov.b64 %{wop[(r, u)]}, {{wl, wh}};")
+                           f"mov.b64 %{wp[((r, u), 0)]}, {{wl, wh}};")
+    else:
+        for i, key in enumerate(wkeys):
+            if NPAIR == 1:
+                asm.append(f"ld.shared.b64 %{wp[(key, 0)]}, [ea+{i * tap_bytes}];")
+            else:
+                asm.append(f"ld.shared.v2.b64 {{%{wp[(key, 0)]}, %{wp[(key, 1)]}}}, [ea+{i * tap_bytes}];")
+            if NSING:
+                asm.append(f"ld.shared.f32 %{ws[key]}, [es+{i * tap_bytes + 256}];")
     asm.append("bra.uni LOOP_%=;")
     asm.append("END_%=:")
     asm.append("}")
@@ -145,24 +187,25 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
     lines.append(f"struct V{vid} {{")
     for k, v in (("R", R), ("S", S), ("P", P), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
                  ("NW", NW), ("MINB", MINB), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
-                 ("NWOPS", len(wops))):
+                 ("NPAIR", NPAIR), ("NSING", NSING), ("NWP", len(wp)), ("NWS", max(1, len(ws)))):
         lines.append(f"    static constexpr int {k} = {v};")
+    lines.append(f"    static constexpr bool XPAIR = {'true' if XPAIR else 'false'};")
     lines.append(f'    static constexpr const char* NAME = "{name}";')
     lines.append(f"    static constexpr int LOADW = {LW}, EXIT = {EXIT};")
     lines.append("    // Run the entry stream at shared address `stream` (see tools/gen_gather.py).")
-    lines.append("    // acc[ty][m], wp[i]: f32x2 bit patterns (x in the low word); wlane: shared")
-    lines.append("    // address of this lane's weights of channel `cbase` (first channel of the stage).")
-    lines.append("    __device__ __forceinline__ static void run(unsigned long long (&acc)[TY][NX], "
-                 "unsigned long long (&wp)[NWOPS], const unsigned stream, const unsigned wlane, "
-                 "const unsigned cbase) {")
+    lines.append("    // accp/wp: f32x2 bit patterns (low word = first element); wlane / wlane_s:")
+    lines.append("    // shared address of this lane's paired / single weights of channel `cbase`.")
+    lines.append("    __device__ __forceinline__ static void run(unsigned long long (&accp)[TY][NX][NPAIR], "
+                 "float (&accs)[TY][NX], unsigned long long (&wp)[NWP], float (&ws)[NWS], const unsigned stream, "
+                 "const unsigned wlane, const unsigned wlane_s, const unsigned cbase) {")
     lines.append("        asm volatile(")
     for a in asm:
         lines.append(f'            "{a}\\n\\t"')
-    outs = ", ".join([f'"+l"(acc[{ty}][{m}])' for (ty, m) in accs] + [f'"+l"(wp[{i}])' for i in range(len(wops))])
-    ins = '"r"(stream), "r"(wlane), "r"(cbase)'
-    lines.append(f"            : {outs}")
-    lines.append(f"            : {ins}")
+    lines.append("            : " + ", ".join(f"{c}({e})" for c, e in ops))
+    lines.append('            : "r"(stream), "r"(wlane), "r"(wlane_s), "r"(cbase)')
     lines.append('            : "memory");')
+    if not NSING:
+        lines.append("        (void)accs; (void)ws;")
     lines.append("    }")
     lines.append("};")
     return "\n".join(lines)
@@ -174,7 +217,6 @@ def main():
     for v in VARIANTS:
         parts.append(gen_variant(*v))
         parts.append("")
-    # selection order = first match wins: measured fastest first
     order = sorted(VARIANTS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
     parts.append("#define SC_GATHER_VARIANTS(X) \\")
     parts.append(" \\\n".join(f"    X(V{v[0]})" for v in order))
@@ -182,6 +224,15 @@ def main():
     with open(OUT, "w") as f:
         f.write("\n".join(parts))
     print("wrote", OUT)
+    # one translation unit per variant (parallel compilation)
+    csrc = os.path.dirname(OUT)
+    for fn in os.listdir(csrc):
+        if fn.startswith("gather_fast_v") and fn.endswith(".cu"):
+            os.remove(os.path.join(csrc, fn))
+    for v in VARIANTS:
+        with open(os.path.join(csrc, f"gather_fast_v{v[0]}.cu"), "w") as f:
+            f.write(f"// Variant V{v[0]} of the register-tile gather kernel (see gather_fast_impl.cuh).\n"
+                    f"#include \"gather_fast_impl.cuh\"\nSC_INSTANTIATE_VARIANT(V{v[0]})\n")
 
 
 if __name__ == "__main__":

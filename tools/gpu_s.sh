@@ -1,0 +1,2 @@
+timeout 600 python tools/variant_sweep.py C2 0.95,0.99 "12 11 10 7" > gpurun_out/sweep.log 2>&1; echo sweep=$?
+bash tools/gpu_n.sh 11 C2 0.99 v11_99

@@ -46,6 +46,19 @@ def gen(style, TY):
         tail = ["mov.b32 xc, x1;", "mov.b32 cc, c1;", "ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;",
                 "mov.b64 vv, {xc, xc};", "brx.idx.uni cc, TS_%=;"]
         a += tail
+    elif style == "shfl":
+        a += ["ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;", "LOOP_%=:", "mov.b32 xc, x1;",
+              "shfl.sync.idx.b32 cc, c1, 0, 31, -1;", "ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;",
+              "mov.b64 vv, {xc, xc};",
+              "TS_%=: .branchtargets " + ", ".join(labels) + ";", "brx.idx.uni cc, TS_%=;"]
+        tail = ["bra.uni LOOP_%=;"]
+    elif style == "brxinv":
+        # loop-invariant jump index (kernel argument): LDC can leave the loop
+        a += ["ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;", "LOOP_%=:", "mov.b32 xc, x1;",
+              "mov.b32 cc, c1;", "ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;", "mov.b64 vv, {xc, xc};",
+              f"setp.ge.u32 pp, cc, {len(cs)};", "@pp bra.uni END_%=;",
+              "TS_%=: .branchtargets " + ", ".join(labels) + ";", f"brx.idx.uni %{vop + 1}, TS_%=;"]
+        tail = ["bra.uni LOOP_%=;"]
     elif style == "nobrx":
         a += ["ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;", "LOOP_%=:", "mov.b32 xc, x1;",
               "mov.b32 cc, c1;", "ld.shared.v2.b32 {x1, c1}, [ep];", "add.u32 ep, ep, 8;", "mov.b64 vv, {xc, xc};",
@@ -69,7 +82,7 @@ def gen(style, TY):
     NT = {3: 512, 5: 384, 7: 256}[TY]
     nf = sum(len(b) for b in cs)
     src = f'''
-extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const uint2* __restrict__ g_ent, int n, float* out, int nwarps) {{
+extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const uint2* __restrict__ g_ent, int n, float* out, int nwarps, unsigned fixed) {{
   extern __shared__ uint2 ent[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < n + 2; i += blockDim.x) ent[i] = g_ent[i];
@@ -80,7 +93,7 @@ extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const uint2* __rest
   for (int i = 0; i < 9; ++i) w[i] = 0x3f8000003f800000ull + lane + i;
   unsigned s = (unsigned)__cvta_generic_to_shared(ent);
   for (int rep = 0; rep < 8; ++rep)
-  asm volatile("{body}" : {outs} : "r"(s) : "memory");
+  asm volatile("{body}" : {outs} : "r"(s), "r"(fixed) : "memory");
   float r = 0; for (int i = 0; i < {nacc}; ++i) r += __uint_as_float((unsigned)acc[i]);
   out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }}
@@ -93,11 +106,11 @@ def main():
            "#include <cuda_runtime.h>"]
     ents = []
     for TY in (3, 5, 7):
-        for style in ("loop", "threaded", "nobrx"):
+        for style in ("loop", "shfl", "brxinv", "nobrx"):
             name, s, nc, nf, nt = gen(style, TY)
             src.append(s)
             ents.append(f'{{{nc}, {nf}, {name}, "{name}", {nt}}}')
-    src.append("typedef void (*kfn)(const uint2*, int, float*, int);")
+    src.append("typedef void (*kfn)(const uint2*, int, float*, int, unsigned);")
     src.append("struct C { int nc, nf; kfn k; const char* name; int nt; };")
     src.append("C cs[] = {" + ", ".join(ents) + "};")
     src.append(r'''
@@ -120,9 +133,9 @@ int main() {
     cudaFuncSetAttribute(c.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
     for (int wps : {1, 2, 3, 4}) {
       int nw = wps * 4; if (nw * 32 > c.nt) continue;
-      c.k<<<148, c.nt, (n + 2) * 8>>>(d_ent, n, d_out, nw);
+      c.k<<<148, c.nt, (n + 2) * 8>>>(d_ent, n, d_out, nw, (unsigned)(c.nc / 2));
       cudaEventRecord(e0);
-      c.k<<<148, c.nt, (n + 2) * 8>>>(d_ent, n, d_out, nw);
+      c.k<<<148, c.nt, (n + 2) * 8>>>(d_ent, n, d_out, nw, (unsigned)(c.nc / 2));
       cudaEventRecord(e1);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
