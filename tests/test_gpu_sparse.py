@@ -179,7 +179,11 @@ def test_subnormal_inputs_count_as_nonzero(sc):
     torch.cuda.synchronize()
     check_lists(conv, x, 1)
     st = conv.lists(1)
-    assert int(st["offs"][0, :, -1].sum()) == shp.c * st["tiles"] + 1   # markers + the subnormal
+    # markers + the subnormal once per tile window that holds input row 5 (R9)
+    lo = np.arange(st["tiles"]) * st["ty"] * shp.stride - shp.pad
+    in_windows = int(((lo <= 5) & (5 < lo + st["nwr"])).sum())
+    assert in_windows >= 1
+    assert int(st["offs"][0, :, -1].sum()) == shp.c * st["tiles"] + in_windows
     ws = np.full_like(w, 2.0 ** 100)
     conv2 = make_conv(sc, shp, ws, None)
     out = conv2.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
@@ -265,21 +269,27 @@ def test_c5_chain_per_layer(sc):
         xd = out
 
 
-@pytest.mark.parametrize("variant", [0, 1, 6])
+FORCED = [("C2", v) for v in (0, 1, 7, 10, 11, 12, 13)] + [("C4a", v) for v in (0, 2, 14)]
+
+
+@pytest.mark.parametrize("cfg,variant", FORCED)
 @pytest.mark.parametrize("s", [0.0, 0.95])
-def test_forced_variants_c2(sc, variant, s, monkeypatch):
-    """Every stage-2 kernel that matches C2 (generic=0, KL=2 tiles, KL=1 whole
-    plane) against the oracle, via SC_FORCE_VARIANT."""
+def test_forced_variants(sc, cfg, variant, s, monkeypatch):
+    """Every stage-2 kernel that matches C2 / C4a (generic = 0, and each
+    generated register-tile variant of tools/gen_gather.py) against the
+    oracle via SC_FORCE_VARIANT: tolerance on seeded data (dense s=0 too) and
+    bit-exact on integer data."""
     monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
-    shp = datagen.C2.with_batch(5)
+    shp = datagen.CONFIGS[cfg].with_batch(5)
     x = datagen.activations(shp, s, seed=3)
     w, b = datagen.weights(shp, seed=3)
     conv = make_conv(sc, shp, w, b, max_batch=9)
     assert conv.variant[0] == variant
     out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    check_lists(conv, x, 5)
     check_conv(out, x, w, b, shp)
     xi, wi, bi = datagen.integer_case(shp, sparsity=0.7)
     conv = make_conv(sc, shp, wi, bi, max_batch=9)
     out = conv.forward(torch.from_numpy(xi).to(DEV)).cpu().numpy()
-    ref, _ = oracle.conv_fp64(xi, wi, bi, 1, 1, 1)
+    ref, _ = oracle.conv_fp64(xi, wi, bi, shp.stride, shp.pad, shp.groups)
     assert np.array_equal(out.astype(np.float64), ref)

@@ -1,2 +1,1 @@
-timeout 600 python tools/variant_sweep.py C2 0.95,0.99 "12 11 10 7" > gpurun_out/sweep.log 2>&1; echo sweep=$?
-bash tools/gpu_n.sh 11 C2 0.99 v11_99
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
