@@ -2,23 +2,29 @@
 """bench.py -- headline benchmark of the ReLU-sparse convolution (arXiv 1704.07724).
 
 Metric (BASELINE.json): sparse conv dense-equivalent GFLOP/s (and nonzero-MAC/s,
-% roofline) at s = 0.9 / 0.95 / 0.99.  Workload (BASELINE.json configs[1], the
-config the metric is quoted on): AlexNet conv3, N=128 images per GPU,
-256x13x13 -> 384 filters 3x3, pad 1, stride 1, fp32, i.i.d. Bernoulli(1-s) *
-|N(0,1)| activations; the headline line is s = 0.95.
+% roofline) at s = 0.9 / 0.95 / 0.99.  Default workload (BASELINE.json
+configs[1], the config the metric is quoted on): AlexNet conv3, N=128 images per
+GPU, 256x13x13 -> 384 filters 3x3, pad 1, stride 1, fp32, i.i.d.
+Bernoulli(1-s) * |N(0,1)| activations; the headline line is s = 0.95 and the
+other two sparsities are reported under "sweep".
 
 A "step" = one sparse_conv_forward (stage 1 compaction + stage 2 gather conv)
-over the 128-image batch, inputs resident in HBM.  Steps rotate over several
-input/output sets whose total (>= 220 MB) exceeds the 126 MB L2.  Each step is
-one CUDA-graph replay (graph captured around the C-ABI call) so host launch
-latency does not leak into the device time.
+over the batch, inputs resident in HBM.  Steps rotate over several input/output
+sets whose total exceeds 2x the 126 MB L2.  Each step is one CUDA-graph replay
+(captured around the C-ABI call).  Per-stage device times come from graphs
+holding REPS back-to-back launches (host launch cost excluded).
+
+--config C5: the AlexNet conv3->conv4->conv5 chain (BASELINE.json configs[4]),
+N=1024 images split over the ranks (strong scaling), ReLU fused into the
+epilogues of conv3/conv4; a step = the three layers.
 
 Usage:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--sparsity S] [--config C2]
   python bench.py --impl reference ...   (the CPU oracle as the reference arm)
-Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (weak scaling: each
-rank processes its own 128 images, batch-sharded by global image index; no
-collective on the data path, P:71 -- images are independent).
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N.  C2 etc.: weak
+scaling, each rank its own 128 images (global image index, shard-independent
+data); C5: the 1024-image batch is sharded.  No collective on the data path
+(images are independent); NCCL only for barriers and max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -35,12 +41,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1704_07724_b200 import datagen  # noqa: E402
+from paper_1704_07724_b200 import datagen, shard  # noqa: E402
 
 METRIC = "sparse conv dense-equiv GFLOP/s & nonzero-MAC/s at s=0.9/0.95/0.99; % roofline"
 SM_COUNT = 148
-FMA_PER_CLK_PER_SM = 128          # FP32 lanes per SM (B200), DESIGN.md "Roofline"
+FMA_PER_CLK_PER_SM = 128          # FP32 lanes per SM (B200), DESIGN.md "Kernels and their rooflines"
 F_MAX_GHZ = 1.965                 # clocks.max.sm
+FP32_PEAK_TFLOPS = SM_COUNT * FMA_PER_CLK_PER_SM * 2 * F_MAX_GHZ / 1e3   # 74.4
+REPS = 20                         # launches per stage-timing graph
 
 
 def measured_peaks():
@@ -49,6 +57,15 @@ def measured_peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def measured_traffic(variant_name):
+    """DRAM bytes per gather launch from the committed ncu capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_traffic.json")) as f:
+            return json.load(f).get(variant_name)
+    except OSError:
+        return None
 
 
 # ------------------------------------------------------------------ counting
@@ -64,23 +81,37 @@ def coverage(extent_in, k, stride, pad, extent_out):
 
 
 def mac_counts(x, shp):
-    """dense MACs and exact nonzero MACs of one batch."""
-    dense = x.shape[0] * shp.ho * shp.wo * shp.r * shp.s * shp.k * (shp.c // shp.groups)
+    """dense MACs, exact nonzero MACs and nnz of one batch
+    (x: numpy or torch tensor; counted on its device)."""
+    n = x.shape[0]
+    dense = n * shp.ho * shp.wo * shp.r * shp.s * shp.k * (shp.c // shp.groups)
     ch = coverage(shp.h, shp.r, shp.stride, shp.pad, shp.ho)
     cw = coverage(shp.w, shp.s, shp.stride, shp.pad, shp.wo)
-    per_pos = (x != 0).sum(axis=(0, 1)).astype(np.int64)
+    if isinstance(x, np.ndarray):
+        per_pos = (x != 0).sum(axis=(0, 1)).astype(np.int64)
+        nnz = int(np.count_nonzero(x))
+    else:
+        per_pos = (x != 0).sum(dim=(0, 1)).cpu().numpy().astype(np.int64)
+        nnz = int((x != 0).sum().item())
     exact = int((shp.k // shp.groups) * (ch[:, None] * cw[None, :] * per_pos).sum())
-    return dense, exact, int(np.count_nonzero(x))
+    return dense, exact, nnz
 
 
-def algorithmic_bytes(shp, n, nnz, idx_bytes, num_lists):
+def algorithmic_bytes(shp, n, nnz, num_lists):
     """Two-stage minimum traffic: dense in + dense out + weights + bias
-    + compacted lists written once and read once."""
+    + compacted lists written once and read once (8 B per entry: value + position,
+    one marker per list, reading R9)."""
     dense_in = 4 * n * shp.c * shp.h * shp.w
     dense_out = 4 * n * shp.k * shp.ho * shp.wo
     wts = 4 * shp.k * (shp.c // shp.groups) * shp.r * shp.s + 4 * shp.k
-    lists = nnz * (4 + idx_bytes) + 4 * num_lists
-    return dense_in + dense_out + wts + 2 * lists, dense_in, lists
+    lists = 8 * (nnz + num_lists)
+    return dense_in + dense_out + wts + 2 * lists
+
+
+def roofline_times(exact, nbytes, hbm_gbs):
+    t_fp32 = exact / (FP32_PEAK_TFLOPS / 2 * 1e12)
+    t_hbm = nbytes / (hbm_gbs * 1e9)
+    return t_fp32, t_hbm, max(t_fp32, t_hbm)
 
 
 # ------------------------------------------------------------------ clocks
@@ -138,37 +169,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
-def workload_name(shp, s):
-    return (f"{shp.name}: N={shp.n}/GPU, {shp.c}x{shp.h}x{shp.w} -> {shp.k} {shp.r}x{shp.s} "
+def workload_name(shp, s, n):
+    return (f"{shp.name}: N={n}/GPU, {shp.c}x{shp.h}x{shp.w} -> {shp.k} {shp.r}x{shp.s} "
             f"stride {shp.stride} pad {shp.pad} groups {shp.groups}, s={s}")
-
-
-def cpu_oracle_rate(shp, x_imgs, w, b, min_s=10.0, max_s=30.0):
-    """Time the fp64 oracle (as it stands) on host cores; repeat passes over the
-    given images until >= min_s.  Returns (dense-equiv GFLOP/s, images, seconds)."""
-    import oracle  # the one product-side place the oracle may run (cpu_baseline leg)
-    oracle.build()
-    per_img_flops = 2 * shp.ho * shp.wo * shp.r * shp.s * shp.k * (shp.c // shp.groups)
-    t0 = time.perf_counter()
-    done = 0
-    i = 0
-    while True:
-        xi = x_imgs[i % x_imgs.shape[0]: i % x_imgs.shape[0] + 1]
-        oracle.conv_fp64(xi, w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
-        done += 1
-        i += 1
-        el = time.perf_counter() - t0
-        if el >= min_s or (el >= max_s * 0.5 and done >= 1):
-            break
-    el = time.perf_counter() - t0
-    return per_img_flops * done / el / 1e9, done, el
 
 
 def host_cores():
@@ -178,38 +181,79 @@ def host_cores():
         return os.cpu_count()
 
 
+def per_image_flops(shp):
+    return 2 * shp.ho * shp.wo * shp.r * shp.s * shp.k * (shp.c // shp.groups)
+
+
+def cpu_oracle_rate(layers, x_imgs, weights, min_s=10.0, max_s=30.0):
+    """Time the fp64 oracle (as it stands) on host cores, one image at a time
+    through every layer, until >= min_s.  Returns (dense-equiv GFLOP/s, images, s)."""
+    import oracle  # the one product-side place the oracle may run (cpu_baseline leg)
+    oracle.build()
+    flops = sum(per_image_flops(shp) for shp in layers)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        xi = x_imgs[done % x_imgs.shape[0]: done % x_imgs.shape[0] + 1]
+        for li, shp in enumerate(layers):
+            w, b = weights[li]
+            y, _ = oracle.conv_fp64(xi, w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
+            xi = np.maximum(y, 0.0).astype(np.float32) if li + 1 < len(layers) else None
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= min_s or el >= max_s:
+            break
+    el = time.perf_counter() - t0
+    return flops * done / el / 1e9, done, el
+
+
+def layers_for(config):
+    if config == "C5":
+        return list(datagen.C5_LAYERS), datagen.c5_weights(), datagen.C5_FIRST_SPARSITY
+    shp = datagen.CONFIGS[config]
+    return [shp], [datagen.weights(shp)], None
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    ws, rank, _ = dist_env()
+    ws, rank, _ = shard.dist_env()
     if rank != 0:
         return 0
-    shp = datagen.CONFIGS[args.config]
-    s = args.sparsity
-    w, b = datagen.weights(shp)
+    layers, weights, s_first = layers_for(args.config)
+    s = s_first if s_first is not None else args.sparsity
     import oracle
     oracle.build()
-    per_img_flops = 2 * shp.ho * shp.wo * shp.r * shp.s * shp.k * (shp.c // shp.groups)
-    # bounded sample per step: images chosen so one step takes ~1-3 s of CPU work
-    x = datagen.activations(shp, s, start=0, count=8)
+    flops_img = sum(per_image_flops(shp) for shp in layers)
+    x = datagen.activations(layers[0], s, start=0, count=8)
+
+    def one(xs):
+        for li, shp in enumerate(layers):
+            w, b = weights[li]
+            y, _ = oracle.conv_fp64(xs, w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
+            xs = np.maximum(y, 0.0).astype(np.float32) if li + 1 < len(layers) else None
+
     t0 = time.perf_counter()
-    oracle.conv_fp64(x[:1], w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
+    one(x[:1])
     t1 = time.perf_counter() - t0
-    m = int(max(1, min(8, 2.0 // max(t1, 1e-3))))
+    m = int(max(1, min(8, 2.0 // max(t1, 1e-3))))   # ~1-2 s of CPU work per step
     xs = x[:m]
     for _ in range(args.warmup):
-        oracle.conv_fp64(xs, w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
+        one(xs)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.conv_fp64(xs, w, b, shp.stride, shp.pad, shp.groups, want_mass=False)
+        one(xs)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
-    value = per_img_flops * m * len(times) / tot / 1e9
-    sample = f"{m} of the {shp.n} images of the workload per step (fp64 oracle, OpenMP), {args.steps} steps"
+    value = flops_img * m * len(times) / tot / 1e9
+    n_img = layers[0].n
+    sample = (f"{m} of the {n_img} images of the workload per step through "
+              f"{'the 3-layer chain' if len(layers) > 1 else 'the layer'} (fp64 oracle, OpenMP), {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(shp, s)},
+            "higher_is_better": True, "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(layers[0], s, n_img)},
             "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": host_cores(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -218,43 +262,67 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args):
-    import torch
-    ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    torch.cuda.set_device(dev)
-    from paper_1704_07724_b200 import sparseconv as sc
+def graph_time_us(torch, stream, fn, reps=REPS):
+    """Device time of fn from a CUDA graph of `reps` back-to-back calls."""
+    with torch.cuda.stream(stream):
+        fn()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        b.synchronize()
+    return a.elapsed_time(b) * 1e3 / reps
 
+
+def timed_steps(torch, stream, graphs, steps, warmup, ws, dev):
+    """W untimed + K timed replays (rotating over graphs), barrier + sync on both
+    sides, CUDA events on the launching stream, max over ranks."""
+    with torch.cuda.stream(stream):
+        for i in range(warmup):
+            graphs[i % len(graphs)].replay()
+        stream.synchronize()
+        shard.barrier(ws)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            graphs[i % len(graphs)].replay()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize(dev)
+    return shard.max_over_ranks(e0.elapsed_time(e1), ws, dev) / steps
+
+
+def run_single(args, torch, dev, ws, rank, sc):
     shp = datagen.CONFIGS[args.config]
-    s_head = args.sparsity
     n = shp.n
     w, b = datagen.weights(shp)                     # same seed on every rank: replicated weights
     conv = sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), n, shp.c, shp.h, shp.w,
                          shp.stride, shp.pad, shp.groups)
-    launches_per_step = conv.launch_counts[0]
-    peaks, peak_kind = measured_peaks()
-    hbm_gbs = float(peaks.get("hbm_gbs", 6650.0))
-    fp32_peak_tflops = SM_COUNT * FMA_PER_CLK_PER_SM * 2 * F_MAX_GHZ / 1e3   # 74.4
+    lists_per_batch = n * conv.lists(1)["tiles"] * shp.c
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    stream = torch.cuda.Stream(dev)
 
-    def measure(s, steps, warmup, sets_min_bytes=2 * 126 * 2 ** 20, main=False):
+    def measure(s, steps, warmup):
         per_set = 4 * n * (shp.c * shp.h * shp.w + shp.k * shp.ho * shp.wo)
-        nsets = max(2, -(-max(sets_min_bytes, 2 * l2_bytes) // per_set))
+        nsets = max(2, -(-2 * max(l2_bytes, 126 * 2 ** 20) // per_set))
         xs, outs, counts = [], [], []
         for si in range(nsets):
-            start = (si * ws + rank) * n                     # global image index (shard-independent data)
-            xh = datagen.activations(shp, s, start=start, count=n)
-            counts.append(mac_counts(xh, shp))
-            xs.append(torch.from_numpy(xh).to(dev))
+            start = shard.image_start(si, rank, ws, n)   # global image index: shard-independent data
+            xd = torch.from_numpy(datagen.activations(shp, s, start=start, count=n)).to(dev)
+            counts.append(mac_counts(xd, shp))
+            xs.append(xd)
             outs.append(torch.empty((n, shp.k, shp.ho, shp.wo), device=dev))
-        stream = torch.cuda.Stream(dev)
-        graphs, graphs_gather, graphs_compact = [], [], []
+        graphs = []
         with torch.cuda.stream(stream):
-            for si in range(nsets):            # eager warm-up once per set (also sets kernel attributes)
+            for si in range(nsets):
                 conv.forward(xs[si], outs[si], stream=stream)
             stream.synchronize()
             for si in range(nsets):
@@ -262,144 +330,201 @@ def run_ours(args):
                 with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
                     conv.forward(xs[si], outs[si], stream=stream)
                 graphs.append(g)
-            g1 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g1, stream=stream, capture_error_mode="relaxed"):
-                conv.compact(xs[0], stream=stream)
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2, stream=stream, capture_error_mode="relaxed"):
-                conv.gather(n, outs[0], stream=stream)
-        res = {}
-        with torch.cuda.stream(stream):
-            for i in range(warmup):
-                graphs[i % nsets].replay()
-            stream.synchronize()
-            if ws > 1:
-                torch.distributed.barrier()
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for i in range(steps):
-                graphs[i % nsets].replay()
-            e1.record(stream)
-            e1.synchronize()
-            torch.cuda.synchronize(dev)
-            elapsed_ms = e0.elapsed_time(e1)
-            if ws > 1:
-                t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-                elapsed_ms = float(t.item())
-                torch.distributed.barrier()
-            res["ms_per_step"] = elapsed_ms / steps
-            # per-stage durations on the launching stream (gather = the dominant kernel):
-            # set 0's lists are rebuilt by the compaction graph before the gather graph runs
-            reps = max(steps, 50)
-            g1.replay()
-            stream.synchronize()
-            for name, g in (("gather", g2), ("compact", g1)):
-                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a0.record(stream)
-                for _ in range(reps):
-                    g.replay()
-                a1.record(stream)
-                a1.synchronize()
-                res[f"{name}_us"] = a0.elapsed_time(a1) * 1e3 / reps
+        res = {"ms_per_step": timed_steps(torch, stream, graphs, steps, warmup, ws, dev)}
+        res["compact_us"] = graph_time_us(torch, stream, lambda: conv.compact(xs[0], stream=stream))
+        res["gather_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
+        res["dense_tc_us"] = graph_time_us(torch, stream, lambda: conv.dense_forward(xs[0], outs[0], stream=stream),
+                                           reps=5)
         dense = sum(c[0] for c in counts) / nsets
         exact = sum(c[1] for c in counts) / nsets
         nnz = sum(c[2] for c in counts) / nsets
-        res.update(dense=dense, exact=exact, nnz=nnz, exact_set0=counts[0][1], nsets=nsets,
-                   realized_s=1 - nnz / (n * shp.c * shp.h * shp.w))
-        del graphs, graphs_gather, graphs_compact, g1, g2
+        res.update(dense=dense, exact=exact, nnz=nnz, exact_set0=counts[0][1], nnz_set0=counts[0][2], nsets=nsets,
+                   set_mib=nsets * per_set / 2 ** 20, realized_s=1 - nnz / (n * shp.c * shp.h * shp.w))
+        del graphs
         return res
 
+    return shp, n, conv, lists_per_batch, measure
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = shard.dist_env()
+    dev = shard.init(ws, local)
+    from paper_1704_07724_b200 import sparseconv as sc
+
+    peaks, peak_kind = measured_peaks()
+    hbm_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    if args.config == "C5":
+        return run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind)
+    shp, n, conv, lists_per_batch, measure = run_single(args, torch, dev, ws, rank, sc)
+    s_head = args.sparsity
     clocks = ClockSampler(dev.index)
     with clocks:
-        head = measure(s_head, args.steps, args.warmup, main=True)
+        head = measure(s_head, args.steps, args.warmup)
         sweep = {}
         if not args.no_sweep:
             for s in (0.9, 0.95, 0.99):
-                if abs(s - s_head) < 1e-9:
-                    continue
-                sweep[s] = measure(s, max(args.steps, 20), max(args.warmup, 3))
-        # clocks need a long enough loaded window: keep replaying the headline workload ~0.5 s
-        if head["ms_per_step"] * args.steps < 300.0:
-            measure(s_head, int(400.0 / max(head["ms_per_step"], 1e-3)) + 1, 3)
+                if abs(s - s_head) > 1e-9:
+                    sweep[s] = measure(s, max(args.steps, 20), max(args.warmup, 3))
 
     # --- end to end through the public API with host buffers (pinned) -------------
-    xh = datagen.activations(shp, s_head, start=rank * n, count=n)
+    xh = datagen.activations(shp, s_head, start=shard.image_start(0, rank, ws, n), count=n)
     h_in = torch.from_numpy(xh).pin_memory()
     h_out = torch.empty((n, shp.k, shp.ho, shp.wo)).pin_memory()
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
         conv.forward_host(h_in, h_out)
-    if ws > 1:
-        torch.distributed.barrier()
+    shard.barrier(ws)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         conv.forward_host(h_in, h_out)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = shard.max_over_ranks((time.perf_counter() - t0) / e2e_steps, ws, dev)
 
     def gflops(dense, ms):
         return 2 * dense * ws / (ms * 1e-3) / 1e9
 
+    def summary(r):
+        nbytes = algorithmic_bytes(shp, n, r["nnz"], lists_per_batch)
+        t_fp32, t_hbm, t_roof = roofline_times(r["exact"], nbytes, hbm_gbs)
+        return nbytes, t_fp32, t_hbm, t_roof
+
     v = head
     value = gflops(v["dense"], v["ms_per_step"])
-    nz_rate = v["exact"] * ws / (v["ms_per_step"] * 1e-3)
-    idx_bytes = 1
-    lists = n * shp.c * 1
-    tot_bytes, _, _ = algorithmic_bytes(shp, n, v["nnz"], idx_bytes, lists)
-    t_fp32 = v["exact"] / (fp32_peak_tflops / 2 * 1e12)
-    t_hbm = tot_bytes / (hbm_gbs * 1e9)
-    t_roof = max(t_fp32, t_hbm)
-    # dominant kernel roofline: stage-2 gather, FP32 FMA (ALU) bound
+    nbytes, t_fp32, t_hbm, t_roof = summary(v)
     g_flops = 2 * v["exact_set0"]
     achieved = g_flops / (v["gather_us"] * 1e-6) / 1e12
+    vname = conv.variant[1]
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(v["ms_per_step"], 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(shp, s_head), "global_batch": n * ws, "parallelism": f"dp{ws}",
-                   "l2": f"{v['nsets']} rotating input/output sets ({v['nsets'] * 4 * n * (shp.c * shp.h * shp.w + shp.k * shp.ho * shp.wo) / 2 ** 20:.0f} MiB > L2)",
-                   "timing": "CUDA events around K CUDA-graph replays (one sparse_conv_forward each)",
-                   "realized_sparsity": round(v["realized_s"], 5), "variant": conv.variant[1]},
-        "nonzero_mac_per_s": round(nz_rate, 1),
+        "config": {"workload": workload_name(shp, s_head, n), "global_batch": n * ws, "parallelism": f"dp{ws}",
+                   "l2": f"{v['nsets']} rotating input/output sets ({v['set_mib']:.0f} MiB > 2x L2)",
+                   "timing": "CUDA events around K CUDA-graph replays (one sparse_conv_forward each), max over ranks",
+                   "realized_sparsity": round(v["realized_s"], 5), "variant": vname},
+        "nonzero_mac_per_s": round(v["exact"] * ws / (v["ms_per_step"] * 1e-3), 1),
         "pct_roofline": round(100 * t_roof / (v["ms_per_step"] * 1e-3), 2),
         "roofline_step": {"t_roof_us": round(t_roof * 1e6, 3), "t_fp32_us": round(t_fp32 * 1e6, 3),
-                          "t_hbm_us": round(t_hbm * 1e6, 3), "bytes": int(tot_bytes),
+                          "t_hbm_us": round(t_hbm * 1e6, 3), "bytes": int(nbytes),
                           "exact_nonzero_macs": int(v["exact"]), "dense_macs": int(v["dense"])},
-        "roofline": {"kernel": "gather (stage 2)", "bound": "alu", "achieved": round(achieved, 3),
-                     "peak": round(fp32_peak_tflops, 2), "unit": "TFLOP/s", "frac": round(achieved / fp32_peak_tflops, 4),
-                     "traffic": None,
+        "roofline": {"kernel": f"gather (stage 2, {vname})", "bound": "alu", "achieved": round(achieved, 3),
+                     "peak": round(FP32_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
+                     "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": measured_traffic(vname),
+                     "per_launch": "2 x exact nonzero MACs of one 128-image batch",
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (unit counts x max clock)"},
         "stages_us": {"compact": round(v["compact_us"], 3), "gather": round(v["gather_us"], 3)},
         "compact_hbm": {"achieved_gbs": round(4 * n * shp.c * shp.h * shp.w / (v["compact_us"] * 1e-6) / 1e9, 1),
                         "peak_gbs": hbm_gbs, "peak_kind": peak_kind},
+        "dense_tc": {"us": round(v["dense_tc_us"], 3), "gflops": round(gflops(v["dense"], v["dense_tc_us"] / 1e3), 2),
+                     "sparse_speedup": round(v["dense_tc_us"] / (v["ms_per_step"] * 1e3), 3),
+                     "note": "in-library tcgen05 TF32 implicit-GEMM conv (dense_conv_forward) on the same batch"},
         "sweep": {str(s): {"value": round(gflops(r["dense"], r["ms_per_step"]), 2),
                            "nonzero_mac_per_s": round(r["exact"] * ws / (r["ms_per_step"] * 1e-3), 1),
                            "ms_per_step": round(r["ms_per_step"], 5),
-                           "pct_roofline": round(100 * max(r["exact"] / (fp32_peak_tflops / 2 * 1e12),
-                                                           algorithmic_bytes(shp, n, r["nnz"], 1, lists)[0] /
-                                                           (hbm_gbs * 1e9)) / (r["ms_per_step"] * 1e-3), 2),
-                           "gather_us": round(r["gather_us"], 3), "compact_us": round(r["compact_us"], 3)}
+                           "pct_roofline": round(100 * summary(r)[3] / (r["ms_per_step"] * 1e-3), 2),
+                           "gather_frac_fp32": round(2 * r["exact_set0"] / (r["gather_us"] * 1e-6) / 1e12
+                                                     / FP32_PEAK_TFLOPS, 4),
+                           "gather_us": round(r["gather_us"], 3), "compact_us": round(r["compact_us"], 3),
+                           "dense_tc_speedup": round(r["dense_tc_us"] / (r["ms_per_step"] * 1e3), 3)}
                   for s, r in sweep.items()},
         "e2e": {"value": round(gflops(v["dense"], e2e_s * 1e3), 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int(h_in.numel() * 4), "d2h_bytes_per_step": int(h_out.numel() * 4),
                 "ms_per_step": round(e2e_s * 1e3, 4), "api": "sparse_conv_forward_host (pinned host buffers)"},
-        "gpu_launches": int(args.steps * launches_per_step),
+        "gpu_launches": int(args.steps * conv.launch_counts[0]),
         "clocks": clocks.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, imgs, secs = cpu_oracle_rate(shp, datagen.activations(shp, s_head, start=0, count=min(n, 16)), w, b)
+        rate, imgs, secs = cpu_oracle_rate([shp], datagen.activations(shp, s_head, start=0, count=min(n, 16)),
+                                           [datagen.weights(shp)])
         line["cpu_baseline"] = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": host_cores(), "kind": "oracle",
                                 "sample": f"{imgs} single-image oracle calls over images 0..15 of the workload "
                                           f"({secs:.1f} s, fp64 7-loop, OpenMP)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    shard.finalize(ws)
+    return 0
+
+
+def run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
+    """C5: conv3 -> ReLU -> conv4 -> ReLU -> conv5 on this rank's share of 1024 images."""
+    layers, weights, s_first = layers_for("C5")
+    n_total = layers[0].n
+    lo, hi = shard.shard_range(n_total, rank, ws)
+    n = hi - lo
+    convs = []
+    for li, shp in enumerate(layers):
+        w, b = weights[li]
+        convs.append(sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), n, shp.c, shp.h,
+                                   shp.w, shp.stride, shp.pad, shp.groups, fuse_relu=li + 1 < len(layers)))
+    x0 = torch.from_numpy(datagen.activations(layers[0], s_first, start=lo, count=n)).to(dev)
+    bufs = [x0] + [torch.empty((n, shp.k, shp.ho, shp.wo), device=dev) for shp in layers]
+    stream = torch.cuda.Stream(dev)
+
+    def step():
+        for li, conv in enumerate(convs):
+            conv.forward(bufs[li], bufs[li + 1], stream=stream)
+
+    with torch.cuda.stream(stream):
+        step()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+            step()
+    counts = [mac_counts(bufs[li], shp) for li, shp in enumerate(layers)]   # realized per-layer inputs
+    clocks = ClockSampler(dev.index)
+    with clocks:
+        ms = timed_steps(torch, stream, [g], args.steps, args.warmup, ws, dev)
+        layer_us = [graph_time_us(torch, stream, (lambda c=conv, a=bufs[li], o=bufs[li + 1]:
+                                                  c.forward(a, o, stream=stream)), reps=5)
+                    for li, conv in enumerate(convs)]
+    dense = sum(c[0] for c in counts)
+    exact = sum(c[1] for c in counts)
+    nbytes = sum(algorithmic_bytes(shp, n, counts[li][2], n * convs[li].lists(1)["tiles"] * shp.c)
+                 for li, shp in enumerate(layers))
+    t_fp32, t_hbm, t_roof = roofline_times(exact, nbytes, hbm_gbs)
+    total_dense = shard.sum_over_ranks(dense, ws, dev)
+    total_exact = shard.sum_over_ranks(exact, ws, dev)
+    value = 2 * total_dense / (ms * 1e-3) / 1e9
+    # e2e through the public API with host buffers: layer by layer, activations stay on the device
+    h_in = torch.from_numpy(x0.cpu().numpy()).pin_memory()
+    h_out = torch.empty(tuple(bufs[-1].shape)).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        bufs[0].copy_(h_in, non_blocking=True)
+        step()
+        h_out.copy_(bufs[-1], non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    with torch.cuda.stream(stream):
+        e2e_step()
+        shard.barrier(ws)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = shard.max_over_ranks((time.perf_counter() - t0) / e2e_steps, ws, dev)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"c5 chain conv3->conv4->conv5, N={n_total} total ({n}/GPU), first input s={s_first}",
+                   "global_batch": n_total, "parallelism": f"dp{ws}", "l2": "inputs larger than L2 (177 MB/GPU at N=1)",
+                   "timing": "CUDA events around K graph replays of the 3-layer chain, max over ranks",
+                   "layer_input_sparsity": [round(1 - c[2] / (n * shp.c * shp.h * shp.w), 4)
+                                            for c, shp in zip(counts, layers)],
+                   "variants": [c.variant[1] for c in convs]},
+        "nonzero_mac_per_s": round(total_exact / (ms * 1e-3), 1),
+        "pct_roofline": round(100 * t_roof / (ms * 1e-3), 2),
+        "layers_us": [round(t, 2) for t in layer_us],
+        "e2e": {"value": round(2 * total_dense / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(h_in.numel() * 4), "d2h_bytes_per_step": int(h_out.numel() * 4),
+                "ms_per_step": round(e2e_s * 1e3, 4)},
+        "gpu_launches": int(args.steps * sum(c.launch_counts[0] for c in convs)),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    shard.finalize(ws)
     return 0
 
 
@@ -409,7 +534,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS) + ["C5"])
     ap.add_argument("--sparsity", type=float, default=0.95)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

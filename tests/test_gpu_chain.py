@@ -1,0 +1,56 @@
+"""C5 (BASELINE.json configs[4]): AlexNet conv3 -> ReLU -> conv4 -> ReLU ->
+conv5 through the C-ABI library with ReLU fused into the epilogue (Eq. 2,
+PAPER.md:77; reading R15).  Parity per layer on the GPU's own input to that
+layer (reading R14): a ReLU threshold near 0 can flip between fp32 and fp64,
+so each layer's oracle sees exactly the tensor the GPU layer saw; ReLU'd
+outputs are compared with max(0, oracle) (max is 1-Lipschitz, the tolerance
+carries over).  Stage-1 lists are checked bit-exactly on the same tensors."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1704_07724_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def run_chain(n, images):
+    from paper_1704_07724_b200 import sparseconv as sc
+    layers = [shp.with_batch(n) for shp in datagen.C5_LAYERS]
+    weights = datagen.c5_weights()
+    x = torch.from_numpy(datagen.activations(layers[0], datagen.C5_FIRST_SPARSITY)).to(DEV)
+    worst = 0.0
+    for li, shp in enumerate(layers):
+        w, b = weights[li]
+        relu = li + 1 < len(layers)
+        conv = sc.SparseConv(torch.from_numpy(w).to(DEV), torch.from_numpy(b).to(DEV), n, shp.c, shp.h, shp.w,
+                             shp.stride, shp.pad, shp.groups, fuse_relu=relu)
+        y = conv.forward(x)
+        torch.cuda.synchronize()
+        xin = x.cpu().numpy()
+        lists = conv.lists(n)
+        ref_l = oracle.compact_streams(xin, shp.r, shp.stride, shp.pad, lists["ty"])
+        assert np.array_equal(lists["offs"].cpu().numpy().view(np.uint32), ref_l["offs"]), f"layer {li} offsets"
+        got = y.cpu().numpy()
+        for i in images:
+            ref, mass = oracle.conv_fp64(xin[i:i + 1], w, b, shp.stride, shp.pad, shp.groups)
+            if relu:
+                ref = np.maximum(ref, 0.0)
+            err = np.abs(got[i:i + 1].astype(np.float64) - ref) / oracle.tolerance_sparse(mass)
+            assert err.max() <= 1.0, f"layer {li} image {i}: max err/tol {err.max():.3f}"
+            worst = max(worst, float(err.max()))
+        if relu:
+            s_next = 1.0 - float((y != 0).sum().item()) / y.numel()
+            assert 0.85 < s_next < 0.995, f"layer {li} output sparsity {s_next}"   # R13 bias shift holds s~0.95
+        x = y
+    return worst
+
+
+def test_c5_chain_small_batch_all_images():
+    run_chain(4, range(4))
+
+
+def test_c5_chain_full_batch_sampled_images():
+    run_chain(1024, [0, 511, 1023])
