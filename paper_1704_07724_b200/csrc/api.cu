@@ -24,6 +24,9 @@ struct sc_plan_s {
     float* bias = nullptr;     // [K]
     uint2* entries = nullptr;  // stage-1 tile streams [N][tiles][cap] (+2 entries of slack)
     uint32_t* offs = nullptr;  // [N][tiles][C+1]
+    uint32_t* cnt = nullptr;   // stage-1 counts [N][tiles][C] (plane-major compaction)
+    uint2* plist = nullptr;    // stage-1 per-plane compacted lists [N*C][H*W]
+    uint32_t* prow = nullptr;  // stage-1 per-plane row prefixes [N*C][H+1]
     int variant = 0;
     const char* variant_name = "generic";
     // staging for sparse_conv_forward_host (allocated on first use)
@@ -149,6 +152,9 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->bias);
     cudaFree(p->entries);
     cudaFree(p->offs);
+    cudaFree(p->cnt);
+    cudaFree(p->plist);
+    cudaFree(p->prow);
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
     delete p;
@@ -224,7 +230,11 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         (e = cudaMalloc(&plan->wdense, dbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
         (e = cudaMalloc(&plan->entries, sizeof(uint2) * (g.N * g.tiles * g.cap + 2))) != cudaSuccess ||
-        (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess) {
+        (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess ||
+        (sc::compact_uses_counts(g) &&
+         ((e = cudaMalloc(&plan->cnt, sizeof(uint32_t) * g.N * g.tiles * g.C)) != cudaSuccess ||
+          (e = cudaMalloc(&plan->plist, sizeof(uint2) * g.N * g.C * g.H * g.W)) != cudaSuccess ||
+          (e = cudaMalloc(&plan->prow, sizeof(uint32_t) * g.N * g.C * (g.H + 1))) != cudaSuccess))) {
         free_plan(plan);
         return cuda_fail(e, "sparse_conv_create: cudaMalloc");
     }
@@ -259,7 +269,7 @@ sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float* d_in, sc_str
     if (st != SC_OK) return st;
     if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
-    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->entries, plan->offs, (cudaStream_t)stream);
+    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, plan->entries, plan->offs, (cudaStream_t)stream);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "compact launch");
 }
 
@@ -342,7 +352,7 @@ sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t* variant, const char*
 
 sc_status sparse_conv_launch_count(sc_plan plan, int32_t* sparse_launches, int32_t* dense_launches) {
     if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
-    if (sparse_launches) *sparse_launches = 2;
+    if (sparse_launches) *sparse_launches = sc::compact_uses_counts(plan->g) ? 3 : 2;
     if (dense_launches) *dense_launches = 1;
     return SC_OK;
 }

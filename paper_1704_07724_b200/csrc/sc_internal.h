@@ -33,8 +33,12 @@ struct DenseGeom {
 cudaError_t launch_pack_weights(const Geometry& g, const float* w, float* wpack, cudaStream_t st);
 cudaError_t launch_pack_dense(const Geometry& g, const DenseGeom& dg, const float* w, float* wdense,
                               cudaStream_t st);
-cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint2* entries, uint32_t* offs,
-                           cudaStream_t st);
+// Stage 1.  The plane-major path (compact_uses_counts) needs workspaces
+// cnt [N][tiles][C] u32, plist [N*C][H*W] (bits, index) pairs and
+// prow [N*C][H+1] u32; they may be null otherwise.
+bool compact_uses_counts(const Geometry& g);
+cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
+                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st);
 cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
                                   const float* wpack, const float* bias, float* out, cudaStream_t st);
 
