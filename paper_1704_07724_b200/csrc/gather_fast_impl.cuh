@@ -293,16 +293,20 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         int rows = TY - r0 < ER ? TY - r0 : ER;
         if (y0 + r0 + rows > a.Ho) rows = a.Ho - (y0 + r0);
         if (rows > 0) {
-            // flattened (channel row kk, pixel p) loop: 32 consecutive elements per step
+            // channel row kk (the channel of lane kk's slot h) is one contiguous run of
+            // rows*WO outputs in NCHW: lanes store consecutive elements of it
             const int len = rows * WO;
             const int nrows = (krows - h + V::KL - 1) / V::KL;  // lanes whose slot h is a valid channel
-            const int total = nrows * len;
-            float* dst0 = a.out + ((size_t)(n * a.K + g * a.Kg + kloc + h) * a.Ho + y0 + r0) * WO;
+            float* dst0 = a.out + ((size_t)(n * a.K + g * a.Kg + kloc + h) * a.Ho + y0 + r0) * WO + lane;
             const size_t kstride = (size_t)a.Ho * WO * V::KL;
+            if (len <= 32) {
+                if (lane < len) {
 #pragma unroll 4
-            for (int idx = lane; idx < total; idx += 32) {
-                const int kk = idx / len, p = idx - kk * len;
-                dst0[kk * kstride + p] = epi[kk * ES + p];
+                    for (int kk = 0; kk < nrows; ++kk) dst0[kk * kstride] = epi[kk * ES + lane];
+                }
+            } else {
+                for (int kk = 0; kk < nrows; ++kk)
+                    for (int p = lane; p < len; p += 32) dst0[kk * kstride + p - lane] = epi[kk * ES + p];
             }
         }
         __syncwarp();
