@@ -51,11 +51,17 @@ VARIANTS = [
     (14, "r3s3p1_w28_ty1_kl4_nw11", 3, 3, 1, 28, 1, 4, 11, 1, 8, 3),  # C4a: k-quads
 ]
 
+# ablations of V12 for timing studies only (wrong results: never selected unless forced)
+ABLATIONS = [
+    (90, "ablate_v12_noload", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3, "noload"),
+    (91, "ablate_v12_nofma", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3, "nofma"),
+]
+
 # selection order = first match wins (measured fastest first)
 PRIORITY = [12, 11, 10, 13, 7, 1, 14, 2]
 
 
-def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
+def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None):
     WO = W + 2 * P - S + 1
     XPAIR = KL == 1
     NX = (WO + 1) // 2 if XPAIR else WO            # accumulator columns per row
@@ -134,6 +140,8 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
                             o, wh = scalar(r, t)
                             body.append(f"mov.b64 {{al, ah}}, %{a}; mov.b64 {{wl, wh}}, %{o}; "
                                         f"fma.rn.f32 a{half}, w{wh[0]}, vf, a{half}; mov.b64 %{a}, {{al, ah}};")
+            if ablate == "nofma" and body:
+                body = ["mov.b32 ea, ea;"]
             bodies.append(body)
             n_fma += len(body)
     # ---- interpreter over a shared-memory entry stream ------------------
@@ -170,7 +178,9 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
         asm.append(f"mad.lo.u32 es, ea, {chb}, %{wsop};")
     asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
     tap_bytes = 32 * KL * 4
-    if XPAIR:
+    if ablate == "noload":
+        pass
+    elif XPAIR:
         for r in range(R):
             for u in range(1, S):
                 # pair (W[r][u], W[r][u-1]); weights of tap (r,t) at byte (r*S+t)*128 + lane*4
@@ -219,10 +229,10 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES):
 def main():
     parts = ["// GENERATED by tools/gen_gather.py -- do not edit.  See that script for the derivation.",
              "#pragma once", ""]
-    for v in VARIANTS:
+    for v in VARIANTS + ABLATIONS:
         parts.append(gen_variant(*v))
         parts.append("")
-    order = sorted(VARIANTS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
+    order = sorted(VARIANTS + ABLATIONS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
     parts.append("#define SC_GATHER_VARIANTS(X) \\")
     parts.append(" \\\n".join(f"    X(V{v[0]})" for v in order))
     parts.append("")
@@ -234,7 +244,7 @@ def main():
     for fn in os.listdir(csrc):
         if fn.startswith("gather_fast_v") and fn.endswith(".cu"):
             os.remove(os.path.join(csrc, fn))
-    for v in VARIANTS:
+    for v in VARIANTS + ABLATIONS:
         with open(os.path.join(csrc, f"gather_fast_v{v[0]}.cu"), "w") as f:
             f.write(f"// Variant V{v[0]} of the register-tile gather kernel (see gather_fast_impl.cuh).\n"
                     f"#include \"gather_fast_impl.cuh\"\nSC_INSTANTIATE_VARIANT(V{v[0]})\n")
