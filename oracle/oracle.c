@@ -103,7 +103,9 @@ int oracle_conv_fp64(const float *in, const float *w, const float *bias,
  * NWIN = NWR*W window positions.  stream[n][t] is a sequence of 8-byte
  * entries (a, b) (u32 pairs):
  *   for c = 0..C-1 (ascending):
- *     marker  (a = c, b = NWIN)
+ *     marker  (a = c, b = NWIN + mask), bit r of mask set iff some entry
+ *             below lies at a window row wi with wi - r = ty*T for a tile
+ *             row 0 <= ty < TY (the filter rows r the channel reaches)
  *     for every input x = in[n,c,i,j] != 0.0f (IEEE compare: -0.0 is zero;
  *     subnormal/NaN/Inf are nonzero) with i inside the window and the plane,
  *     ascending (i, j):  (a = bit copy of x, b = (i - i_lo)*W + j)
@@ -128,8 +130,9 @@ int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int
             for (int64_t c = 0; c < C; ++c) {
                 of[c] = (uint32_t)len;
                 if (len >= cap) { bad = 1; break; }
+                const int64_t marker = len;
+                uint32_t mask = 0;  /* tap rows r reached by this channel's entries */
                 st[2 * len] = (uint32_t)c;
-                st[2 * len + 1] = (uint32_t)NWIN;
                 ++len;
                 for (int64_t wi = 0; wi < NWR; ++wi) {
                     const int64_t i = i_lo + wi;
@@ -143,9 +146,14 @@ int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int
                             st[2 * len] = bits;
                             st[2 * len + 1] = (uint32_t)(wi * W + j);
                             ++len;
+                            for (int64_t r = 0; r < R && r < 32; ++r) {
+                                const int64_t d = wi - r;  /* = ty*T for tile row ty */
+                                if (d >= 0 && d % T == 0 && d / T < TY) mask |= 1u << r;
+                            }
                         }
                     }
                 }
+                st[2 * marker + 1] = (uint32_t)NWIN + mask;
             }
             of[C] = (uint32_t)len;
         }

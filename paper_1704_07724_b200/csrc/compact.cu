@@ -4,9 +4,10 @@
 // and store the non-zero values in a vector with their column and row
 // information".  Output format: reading R9 (include/sparse_conv.h,
 // DESIGN.md): one stream per (image n, output row-tile t) holding, for every
-// input channel c in order, a marker (c, NWIN) followed by the channel's
+// input channel c in order, a marker (c, NWIN + mask) followed by the channel's
 // nonzeros inside the tile's input window as (value bits, window position),
-// ascending; offs[n][t][c] = index of channel c's marker, offs[..][C] = length.
+// ascending; offs[n][t][c] = index of channel c's marker, offs[..][C] = length;
+// bit r of mask = filter row r is reached by one of the channel's entries.
 // The stream is exactly the instruction stream the stage-2 interpreter runs.
 //
 // Design: one CTA per stream, one pass over the data.
@@ -26,6 +27,17 @@ namespace sc {
 
 namespace {
 constexpr int kRegs = 16;  // RCH * KV: values held per lane per round
+
+// Marker mask bits (R9) of one entry at window row wi: filter row r is reached
+// iff wi - r = ty*T for a tile row 0 <= ty < TY.
+__device__ __forceinline__ unsigned tap_rows(unsigned wi, int R, int T, int TY) {
+    unsigned m = 0;
+    for (int r = 0; r < R && r < 32; ++r) {
+        const int d = (int)wi - r;
+        if (d >= 0 && d % T == 0 && d / T < TY) m |= 1u << r;
+    }
+    return m;
+}
 }  // namespace
 
 template <int KV>
@@ -50,6 +62,7 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
     uint2* st = entries + (int64_t)stream * cap;
     uint32_t* of = offs + (int64_t)stream * (C + 1);
     const int per_round = nw * RCH;
+    const int R = NWR - (TY - 1) * T;  // filter rows
 
     uint32_t base = 0;
     for (int cb = 0; cb < C; cb += per_round) {
@@ -135,14 +148,16 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
         for (int q = 0; q < RCH; ++q) {
             const int ch = warp + q * nw;
             if (ch < nround) {
-                uint32_t pos = start_s[ch];
-                if (lane == 0) st[pos] = make_uint2((unsigned)(cb + ch), (unsigned)NWIN);
-                ++pos;
+                const uint32_t pos0 = start_s[ch];
+                uint32_t pos = pos0 + 1;
+                unsigned mask = 0;  // filter rows reached by this channel's entries (R9 marker)
 #pragma unroll
                 for (int u = 0; u < KV; ++u) {
-                    if (v[q][u] != 0.0f)
-                        st[pos + __popc(bal[q][u] & lt)] =
-                            make_uint2(__float_as_uint(v[q][u]), shift + (unsigned)(32 * u + lane));
+                    if (v[q][u] != 0.0f) {
+                        const unsigned code = shift + (unsigned)(32 * u + lane);
+                        st[pos + __popc(bal[q][u] & lt)] = make_uint2(__float_as_uint(v[q][u]), code);
+                        mask |= tap_rows(code / (unsigned)W, R, T, TY);
+                    }
                     pos += __popc(bal[q][u]);
                 }
                 if (seg > BLK) {
@@ -150,11 +165,16 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
                     for (int o0 = BLK; o0 < seg; o0 += 32) {
                         const float x = o0 + lane < seg ? __ldg(src + o0 + lane) : 0.0f;
                         const unsigned b = __ballot_sync(0xffffffffu, x != 0.0f);
-                        if (x != 0.0f)
-                            st[pos + __popc(b & lt)] = make_uint2(__float_as_uint(x), shift + (unsigned)(o0 + lane));
+                        if (x != 0.0f) {
+                            const unsigned code = shift + (unsigned)(o0 + lane);
+                            st[pos + __popc(b & lt)] = make_uint2(__float_as_uint(x), code);
+                            mask |= tap_rows(code / (unsigned)W, R, T, TY);
+                        }
                         pos += __popc(b);
                     }
                 }
+                mask = __reduce_or_sync(0xffffffffu, mask);
+                if (lane == 0) st[pos0] = make_uint2((unsigned)(cb + ch), (unsigned)NWIN + mask);
             }
         }
         base += wsum_s[32];
@@ -189,107 +209,93 @@ static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const
 }
 
 // ---------------------------------------------------------------------------
-// Plane-major path (planes of up to kMaxPlane elements): every plane is read
-// once per kernel instead of once per tile window.
-//  count: one warp per (image, channel) plane: compacts the plane (ballot
-//         ranks, row-major = stream order) into plist[plane] as (bits, flat
-//         index), the exclusive row prefix prow[plane][0..H] (shared atomics +
-//         shuffle scan), and each tile's window count cnt[n][t][c] =
-//         prow[r1] - prow[r0].
+// Plane-major path (planes of up to 32*kMaxSlots elements and at most 31 rows):
+// every plane is read once from HBM and compacted once.
+//  count: one warp per (image, channel) plane.  All loads of the plane are in
+//         flight at once (lanes over the flat plane, NSLOT slots of 32); the
+//         slot ballots stay in registers and give (a) each nonzero's rank ->
+//         plist[plane] = (bits, flat index) in row-major order (= the stream
+//         order), (b) the exclusive row prefix prow[plane][r] = nonzeros
+//         before row r (lane r: popc of the ballot bits below r*W), and (c)
+//         each tile's window count cnt[n][t][c] = prow[r1] - prow[r0].
 //  emit:  one CTA per (image, chunk of 32 channels).  Warp w scans tiles
 //         w, w+NW, ...: the chunk's stream base is 1 + count summed over the
 //         channels before it, a shuffle scan over the chunk's channels gives
-//         each marker index (-> offs).  Then every (channel, tile) gets its
-//         marker and the contiguous run plist[prow[r0] .. prow[r1]) of the
-//         plane, positions re-coded relative to the window.
+//         each marker index (-> offs).  Then each warp flattens, per plane,
+//         the (tile, marker / entry) writes into one work list (scan over the
+//         tiles' run lengths) so every lane stores one 8-byte entry per step.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int kMaxPlane = 2048;   // elements per plane on the plane-major path (list: 16 KB/warp)
+constexpr int kMaxSlots = 32;     // plane elements / 32 on the plane-major path
 constexpr int kPlaneWarps = 8;
 constexpr int kPlaneChunk = 32;   // channels per emit CTA
-constexpr int kMaxTiles = 64;
-
-// floor(e / W) for 0 <= e < 2^32 / W: magic = floor(2^32 / W) + 1
-__device__ __forceinline__ unsigned div_w(unsigned e, unsigned magic) { return __umulhi(e, magic); }
+constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 }  // namespace
 
+template <int NSLOT>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
-    const float* __restrict__ in, int planes, int C, int H, int W, unsigned magic, int TYT, int P, int NWR,
-    int tiles, uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow) {
-    extern __shared__ uint32_t rows_s[];  // [kPlaneWarps][H + 1]: nonzeros per row, then prefix
+    const float* __restrict__ in, int planes, int C, int H, int W, int TYT, int P, int NWR, int tiles,
+    uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int plane = blockIdx.x * kPlaneWarps + warp;
     if (plane >= planes) return;
-    uint32_t* rc = rows_s + warp * (H + 1);
-    for (int r = lane; r <= H; r += 32) rc[r] = 0u;
-    __syncwarp();
     const int HW = H * W;
     const float* src = in + (int64_t)plane * HW;
-    uint2* lst = plist + (int64_t)plane * HW;
+    float v[NSLOT];
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u) {
+        const int e = 32 * u + lane;
+        v[u] = e < HW ? __ldg(src + e) : 0.0f;
+    }
     const unsigned lt = (1u << lane) - 1u;
+    uint2* lst = plist + (int64_t)plane * HW;
+    unsigned bal[NSLOT];
     uint32_t total = 0;
-    for (int e0 = 0; e0 < HW; e0 += 128) {
-        float v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = e0 + 32 * u + lane;
-            v[u] = e < HW ? __ldg(src + e) : 0.0f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const unsigned bal = __ballot_sync(0xffffffffu, v[u] != 0.0f);  // IEEE: -0.0 is zero
-            if (v[u] != 0.0f) {
-                const unsigned e = (unsigned)(e0 + 32 * u + lane);
-                lst[total + __popc(bal & lt)] = make_uint2(__float_as_uint(v[u]), e);  // row-major = stream order
-                atomicAdd(&rc[div_w(e, magic) + 1], 1u);
-            }
-            total += __popc(bal);
-        }
+    for (int u = 0; u < NSLOT; ++u) {
+        bal[u] = __ballot_sync(0xffffffffu, v[u] != 0.0f);  // IEEE: -0.0 is zero
+        if (v[u] != 0.0f) lst[total + __popc(bal[u] & lt)] = make_uint2(__float_as_uint(v[u]), 32u * u + lane);
+        total += __popc(bal[u]);
     }
-    __syncwarp();
-    // rc[r] = nonzeros in rows < r (exclusive prefix over H + 1 entries) -> prow
-    uint32_t carry = 0;
-    for (int r0 = 0; r0 <= H; r0 += 32) {
-        const int r = r0 + lane;
-        uint32_t x = r <= H ? rc[r] : 0u;
+    // lane r <= H: nonzeros before element r*W (the first element of row r)
+    const int eb = lane * W;
+    const int sb = eb >> 5;
+    const unsigned mb = (1u << (eb & 31)) - 1u;
+    uint32_t pre = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += u;
-        }
-        x += carry;
-        if (r <= H) {
-            rc[r] = x;
-            prow[(int64_t)plane * (H + 1) + r] = x;
-        }
-        carry = __shfl_sync(0xffffffffu, x, 31);
-    }
-    __syncwarp();
+    for (int u = 0; u < NSLOT; ++u) pre += u < sb ? __popc(bal[u]) : (u == sb ? __popc(bal[u] & mb) : 0u);
+    if (lane > H) pre = total;
+    if (lane <= H) prow[(int64_t)plane * (H + 1) + lane] = pre;
     const int n = plane / C, c = plane - (plane / C) * C;
-    for (int t = lane; t < tiles; t += 32) {  // window rows of tile t: [t*TYT - P, + NWR) within the plane
-        const int lo = t * TYT - P;
-        const int r0 = lo < 0 ? 0 : lo, r1 = (lo + NWR < H) ? lo + NWR : H;
-        cnt[((int64_t)n * tiles + t) * C + c] = r1 > r0 ? rc[r1] - rc[r0] : 0u;
-    }
+    // lane t: tile t's window rows [t*TYT - P, + NWR) clipped to the plane
+    const int lo = lane * TYT - P;
+    const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
+    const uint32_t p0 = __shfl_sync(0xffffffffu, pre, r0), p1 = __shfl_sync(0xffffffffu, pre, r1);
+    if (lane < tiles) cnt[((int64_t)n * tiles + lane) * C + c] = r1 > r0 ? p1 - p0 : 0u;
 }
 
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
-    int H, int W, int TYT, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
+    int H, int W, int TY, int T, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
     uint32_t* __restrict__ offs) {
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
-    __shared__ int2 trow_s[kMaxTiles];  // window rows [r0, r1) of tile t within the plane
-    __shared__ uint2* tst_s[kMaxTiles];  // stream base of tile t
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int chunk = blockIdx.x % chunks;
     const int n = blockIdx.x / chunks;
     const int c0 = chunk * kPlaneChunk;
     const int nch = (C - c0) < kPlaneChunk ? (C - c0) : kPlaneChunk;
     const int HW = H * W;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-        const int i_lo = t * TYT - P;
-        trow_s[t] = make_int2(i_lo < 0 ? 0 : i_lo, (i_lo + NWR < H) ? i_lo + NWR : H);
-        tst_s[t] = entries + ((int64_t)n * tiles + t) * cap;
+    // Issue this warp's plane loads (row prefix: lane r = nonzeros before row r;
+    // the first 32 list entries) before the offset phase so their latency overlaps it.
+    constexpr int kPerWarp = kPlaneChunk / kPlaneWarps;
+    uint32_t pv[kPerWarp];
+    uint2 en0[kPerWarp];
+#pragma unroll
+    for (int q = 0; q < kPerWarp; ++q) {
+        const int ch = warp + q * kPlaneWarps;
+        const int plane = n * C + c0 + ch;
+        pv[q] = (ch < nch && lane <= H) ? __ldg(prow + (int64_t)plane * (H + 1) + lane) : 0u;
+        en0[q] = ch < nch ? __ldg(plist + (int64_t)plane * HW + lane) : make_uint2(0u, 0u);
     }
     // ---- stream offsets of this chunk's channels in every tile stream
     for (int t = warp; t < tiles; t += kPlaneWarps) {
@@ -312,31 +318,68 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
         if (lane == nch - 1 && c0 + nch == C) of[C] = start + v;
     }
     __syncthreads();
-    // ---- every (channel, tile): marker + the run of the plane's list inside the window rows.
-    // The plane's row prefix (lanes over rows) and its list (lanes over entries,
-    // 32 per register block) are loaded once; the runs are assembled with shuffles.
-    for (int ch = warp; ch < nch; ch += kPlaneWarps) {
+    const int TYT = TY * T;
+    const int R = NWR - (TY - 1) * T;  // filter rows
+    // lane t: tile t's window rows, stream base and position shift
+    const int lo = lane * TYT - P;
+    const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
+    const unsigned shift_t = (unsigned)(lo * W);  // code = flat index - i_lo*W
+    uint2* st_t = entries + ((int64_t)n * tiles + (lane < tiles ? lane : 0)) * cap;
+#pragma unroll
+    for (int q = 0; q < kPerWarp; ++q) {
+        const int ch = warp + q * kPlaneWarps;
+        if (ch >= nch) break;
         const int plane = n * C + c0 + ch;
         const uint2* lst = plist + (int64_t)plane * HW;
-        const uint32_t* pr = prow + (int64_t)plane * (H + 1);
-        const uint32_t pv = lane <= H ? __ldg(pr + lane) : 0u;  // lane r: nonzeros in rows < r (H < 32)
-        const uint32_t total = H < 32 ? __shfl_sync(0xffffffffu, pv, H) : __ldg(pr + H);
-        for (uint32_t k0 = 0; k0 < total || k0 == 0; k0 += 32) {  // list block [k0, k0 + 32)
-            const uint2 en = k0 + lane < total ? __ldg(lst + k0 + lane) : make_uint2(0u, 0u);
-            for (int t = 0; t < tiles; ++t) {
-                const int2 rr = trow_s[t];
-                uint2* st = tst_s[t];
-                const uint32_t pos = start_s[t][ch] + 1;
-                if (k0 == 0 && lane == 0) st[pos - 1] = make_uint2((unsigned)(c0 + ch), (unsigned)NWIN);
-                // run [a, b) of the list (row prefix values at the window rows)
-                const uint32_t a = H < 32 ? __shfl_sync(0xffffffffu, pv, rr.x) : __ldg(pr + rr.x);
-                const uint32_t b = H < 32 ? __shfl_sync(0xffffffffu, pv, rr.y) : __ldg(pr + rr.y);
-                const unsigned shift = (unsigned)((t * TYT - P) * W);  // code = flat index - i_lo*W
-                // block k0 covers list indices [k0, k0+32): lane l writes entry k0 + l if inside the run
-                const uint32_t k = k0 + lane;
-                if (k >= a && k < b) st[pos + (k - a)] = make_uint2(en.x, en.y - shift);
+        // lane t: run [a, b) of the plane's list inside tile t's window; work = marker + run
+        const uint32_t a = __shfl_sync(0xffffffffu, pv[q], r0), b = __shfl_sync(0xffffffffu, pv[q], r1);
+        const uint32_t len = lane < tiles ? 1u + (r1 > r0 ? b - a : 0u) : 0u;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        const uint32_t wstart = incl - len;                       // first work item of tile t
+        const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t pos_t = lane < tiles ? start_s[lane][ch] : 0u;
+        // marker of tile t (R9): bit r set iff a nonzero row i = i_lo + r + ty*T, 0 <= ty < TY
+        const uint32_t pnext = __shfl_down_sync(0xffffffffu, pv[q], 1);
+        const unsigned rowbits = __ballot_sync(0xffffffffu, lane < H && pnext > pv[q]);
+        unsigned mask_t = 0;
+        for (int r = 0; r < R; ++r)
+            for (int ty = 0; ty < TY; ++ty) {
+                const int i = lo + r + ty * T;
+                if (i >= 0 && i < H && ((rowbits >> i) & 1u)) mask_t |= 1u << r;
             }
-            if (total == 0) break;
+        for (uint32_t w0 = 0; w0 < wtotal; w0 += 32) {
+            const uint32_t w = w0 + lane;
+            // my tile: the last t with wstart[t] <= w (tiles <= 32; wstart ascending)
+            const unsigned le = __ballot_sync(0xffffffffu, lane < tiles && wstart <= w0 + 31u);
+            int t = 0;
+            for (unsigned m = le; m; m &= m - 1) {
+                const int tt = __ffs(m) - 1;
+                if (__shfl_sync(0xffffffffu, wstart, tt) <= w) t = tt;
+            }
+            const uint32_t ws_t = __shfl_sync(0xffffffffu, wstart, t);
+            const uint32_t a_t = __shfl_sync(0xffffffffu, a, t);
+            const uint32_t p_t = __shfl_sync(0xffffffffu, pos_t, t);
+            const unsigned sh = __shfl_sync(0xffffffffu, shift_t, t);
+            uint2* st = reinterpret_cast<uint2*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(st_t), t));
+            const unsigned m_t = __shfl_sync(0xffffffffu, mask_t, t);
+            const uint32_t j = w - ws_t;  // 0 = marker, j >= 1: list entry a_t + j - 1
+            const uint32_t k = a_t + (j > 0 ? j - 1 : 0);
+            // entries 0..31 of the list sit in en0 (lane k holds entry k)
+            const uint2 ek = make_uint2(__shfl_sync(0xffffffffu, en0[q].x, k & 31),
+                                        __shfl_sync(0xffffffffu, en0[q].y, k & 31));
+            if (w < wtotal) {
+                if (j == 0) {
+                    st[p_t] = make_uint2((unsigned)(c0 + ch), (unsigned)NWIN + m_t);
+                } else {
+                    const uint2 e = k < 32 ? ek : __ldg(lst + k);
+                    st[p_t + j] = make_uint2(e.x, e.y - sh);
+                }
+            }
         }
     }
 }
@@ -345,23 +388,26 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
                            uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st) {
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
         return launch_compact_streamwise(g, n, in, entries, offs, st);
-    const unsigned magic = (unsigned)((0x100000000ull / (uint64_t)g.W) + 1ull);
     const int TYT = (int)(g.ty * g.T);
     const int planes = (int)(n * g.C);
-    compact_plane_count_kernel<<<(unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps), kPlaneWarps * 32,
-                                 sizeof(uint32_t) * kPlaneWarps * (g.H + 1), st>>>(
-        in, planes, (int)g.C, (int)g.H, (int)g.W, magic, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt, plist, prow);
+    const unsigned cgrid = (unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps);
+    if (g.H * g.W <= 256)
+        compact_plane_count_kernel<8><<<cgrid, kPlaneWarps * 32, 0, st>>>(
+            in, planes, (int)g.C, (int)g.H, (int)g.W, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt, plist, prow);
+    else
+        compact_plane_count_kernel<kMaxSlots><<<cgrid, kPlaneWarps * 32, 0, st>>>(
+            in, planes, (int)g.C, (int)g.H, (int)g.W, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt, plist, prow);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
     compact_plane_emit_kernel<<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
-        plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, TYT, (int)g.P, (int)g.nwr, (int)g.nwin, (int)g.tiles, g.cap,
-        chunks, entries, offs);
+        plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
+        (int)g.tiles, g.cap, chunks, entries, offs);
     return cudaGetLastError();
 }
 
 bool compact_uses_counts(const Geometry& g) {
-    return g.H * g.W <= kMaxPlane && g.tiles <= kMaxTiles && g.H + 1 <= 1024;
+    return g.H * g.W <= 32 * kMaxSlots && g.tiles <= kMaxTiles && g.H <= 31;
 }
 
 }  // namespace sc

@@ -323,8 +323,15 @@ def test_compact_streams_against_numpy_and_roundtrip(shape, r, stride, pad, ty):
             e = st["entries"][ni, t]
             for ci in range(c):
                 a, b = of[ci], of[ci + 1]
-                assert e[a, 0] == ci and e[a, 1] == nwin
                 vals, codes = ref[(ni, t, ci)]
+                # marker mask: filter rows r reached by some entry (window row wi = r + ty*stride)
+                mask = 0
+                for wi in set((codes // shape[3]).tolist()):
+                    for rr in range(r):
+                        d = wi - rr
+                        if d >= 0 and d % stride == 0 and d // stride < ty:
+                            mask |= 1 << rr
+                assert e[a, 0] == ci and e[a, 1] == nwin + mask
                 assert np.array_equal(e[a + 1:b, 0], vals)
                 assert np.array_equal(e[a + 1:b, 1], codes)
     back = oracle.decompress_streams(st, shape, stride, pad)

@@ -150,17 +150,20 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
     # load the lane's weights of channel x from the weight stage;
     # code == NCASES+1: exit.  The next entry is loaded before the current one
     # is dispatched.
-    LW, EXIT = NCASES, NCASES + 1
+    # marker code = NCASES + mask (R9): bit r = filter row r is reached by one of the
+    # channel's entries; one marker case per mask loads exactly those rows' weights
+    NMASK = 1 << R
+    LW, EXIT = NCASES, NCASES + NMASK
     chb = R * S * 32 * KL * 4   # bytes of one channel in the weight stage
-    asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .pred pm;",
-           ".reg .f32 al, ah, wl, wh, vf;",
+    asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
            f"mov.b32 ep, %{pop};",
            "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
            "LOOP_%=:",
            "mov.b32 xc, xn;", "mov.b32 cc, cn;",
            "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
            "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
-    labels = [f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)] + ["LW_%=", "END_%="]
+    labels = ([f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)] +
+              [f"LW{m}_%=" if m else "LOOP_%=" for m in range(NMASK)] + ["END_%="])
     asm.append("TS_%=: .branchtargets " + ", ".join(labels) + ";")
     asm.append("brx.idx.uni cc, TS_%=;")
     for i, b in enumerate(bodies):
@@ -168,33 +171,33 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
             asm.append(f"C{i}_%=:")
             asm += b
             asm.append("bra.uni LOOP_%=;")
-    asm.append("LW_%=:")
-    # a marker followed by another marker: the channel has no nonzero in this
-    # window -> skip its weight loads (its successor reloads them)
-    asm.append(f"setp.eq.u32 pm, cn, {LW};")
-    asm.append("@pm bra.uni LOOP_%=;")
-    asm.append(f"sub.u32 ea, xc, %{cbop};")
-    if NSING:
-        asm.append(f"mad.lo.u32 es, ea, {chb}, %{wsop};")
-    asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
     tap_bytes = 32 * KL * 4
-    if ablate == "noload":
-        pass
-    elif XPAIR:
-        for r in range(R):
-            for u in range(1, S):
-                # pair (W[r][u], W[r][u-1]); weights of tap (r,t) at byte (r*S+t)*128 + lane*4
-                asm.append(f"ld.shared.f32 wl, [ea+{(r * S + u) * 128}]; ld.shared.f32 wh, [ea+{(r * S + u - 1) * 128}]; "
-                           f"mov.b64 %{wp[((r, u), 0)]}, {{wl, wh}};")
-    else:
-        for i, key in enumerate(wkeys):
-            if NPAIR == 1:
-                asm.append(f"ld.shared.b64 %{wp[(key, 0)]}, [ea+{i * tap_bytes}];")
-            else:
-                asm.append(f"ld.shared.v2.b64 {{%{wp[(key, 0)]}, %{wp[(key, 1)]}}}, [ea+{i * tap_bytes}];")
-            if NSING:
-                asm.append(f"ld.shared.f32 %{ws[key]}, [es+{i * tap_bytes + 256}];")
-    asm.append("bra.uni LOOP_%=;")
+    for m in range(1, NMASK):
+        asm.append(f"LW{m}_%=:")
+        asm.append(f"sub.u32 ea, xc, %{cbop};")
+        if NSING:
+            asm.append(f"mad.lo.u32 es, ea, {chb}, %{wsop};")
+        asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
+        rows = [r for r in range(R) if (m >> r) & 1]
+        if ablate == "noload":
+            pass
+        elif XPAIR:
+            for r in rows:
+                for u in range(1, S):
+                    # pair (W[r][u], W[r][u-1]); weights of tap (r,t) at byte (r*S+t)*128 + lane*4
+                    asm.append(f"ld.shared.f32 wl, [ea+{(r * S + u) * 128}]; ld.shared.f32 wh, [ea+{(r * S + u - 1) * 128}]; "
+                               f"mov.b64 %{wp[((r, u), 0)]}, {{wl, wh}};")
+        else:
+            for i, key in enumerate(wkeys):
+                if key[0] not in rows:
+                    continue
+                if NPAIR == 1:
+                    asm.append(f"ld.shared.b64 %{wp[(key, 0)]}, [ea+{i * tap_bytes}];")
+                else:
+                    asm.append(f"ld.shared.v2.b64 {{%{wp[(key, 0)]}, %{wp[(key, 1)]}}}, [ea+{i * tap_bytes}];")
+                if NSING:
+                    asm.append(f"ld.shared.f32 %{ws[key]}, [es+{i * tap_bytes + 256}];")
+        asm.append("bra.uni LOOP_%=;")
     asm.append("END_%=:")
     asm.append("}")
     lines = [f"// ---- variant {vid}: {name}  (R={R} S={S} P={P} W={W} WO={WO} TY={TY} KL={KL} NX={NX} NW={NW}); "
@@ -206,7 +209,7 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
         lines.append(f"    static constexpr int {k} = {v};")
     lines.append(f"    static constexpr bool XPAIR = {'true' if XPAIR else 'false'};")
     lines.append(f'    static constexpr const char* NAME = "{name}";')
-    lines.append(f"    static constexpr int LOADW = {LW}, EXIT = {EXIT};")
+    lines.append(f"    static constexpr int LOADW = {LW}, EXIT = {EXIT};  // marker codes LOADW + mask, mask < 2^R")
     lines.append("    // Run the entry stream at shared address `stream` (see tools/gen_gather.py).")
     lines.append("    // accp/wp: f32x2 bit patterns (low word = first element); wlane / wlane_s:")
     lines.append("    // shared address of this lane's paired / single weights of channel `cbase`.")
