@@ -76,9 +76,12 @@ typedef struct sc_plan_s *sc_plan;
  * window_width columns, NWIN = marker_code = NWR*W positions.  Its stream
  * (stream id s = n*tiles_per_image + t) is entries[s*stream_capacity*2 ...],
  * a sequence of u32 pairs (a, b):
- *   for every input channel c ascending: the marker (a = c, b = NWIN), then
- *   every input x = in[n,c,i,j] != 0.0f inside the window (ascending i, j)
- *   as (a = bit copy of x, b = (i - (t*TY*stride - pad))*W + j).
+ *   for every input channel c ascending: the marker (a = c, b = NWIN + mask),
+ *   then every input x = in[n,c,i,j] != 0.0f inside the window (ascending
+ *   i, j) as (a = bit copy of x, b = (i - (t*TY*stride - pad))*W + j).
+ *   Bit r of mask is set iff one of the channel's entries sits at a window
+ *   row wi with wi - r = ty*stride for a tile row 0 <= ty < TY (the filter
+ *   rows the channel reaches; mask = 0 iff the channel has no entry).
  * offsets[s*(C+1) + c] = index of channel c's marker, offsets[s*(C+1) + C] =
  * stream length.  Entries beyond the length are undefined. */
 typedef struct {
@@ -90,7 +93,7 @@ typedef struct {
     int32_t tile_rows;
     int32_t window_rows;
     int32_t window_width;
-    int32_t marker_code;
+    int32_t marker_code;       /* NWIN: markers carry NWIN + mask */
 } sc_lists_view;
 
 /* Output shape (N = params.n): out_nchw = {n, k, H_out, W_out}.  Pure host
