@@ -20,8 +20,8 @@
 //    reduction over input channels.
 //  * the unit's stream (per channel: marker, then in-window nonzeros as
 //    (value, window position)) is cut into pieces at weight-chunk boundaries
-//    and every kPiece entries; each piece is bulk-copied (TMA, per-warp
-//    mbarrier) into a kSlots-deep per-warp shared ring, terminated with an EXIT
+//    and every V::PIECE entries; each piece is bulk-copied (TMA, per-warp
+//    mbarrier) into a V::SLOTS-deep per-warp shared ring, terminated with an EXIT
 //    entry and run by the generated threaded interpreter (tools/gen_gather.py):
 //    one brx.idx.uni per entry into code that applies FFMA2/FFMA to exactly the
 //    accumulators the entry reaches; markers reload the lane's weights.
@@ -37,8 +37,8 @@ namespace fast {
 
 #include "gather_variants.inc"
 
-constexpr int kPiece = 254;  // max entries per piece (+ alignment slot + EXIT = 256)
-constexpr int kSlots = 3;    // pieces in flight per warp
+// Per variant (gather_variants.inc): V::PIECE = max entries per piece (+ alignment
+// slot + EXIT), V::SLOTS = pieces in flight per warp.
 
 struct Args {
     const uint2* entries;
@@ -84,19 +84,19 @@ struct Smem {
     static constexpr int KBW = 32 * V::KL;
     static constexpr int kStageFloats = V::CH * V::R * V::S * KBW;
     // The epilogue reuses the warp's own piece slots (all its pieces have been
-    // consumed by then): KBW x kEpiStride floats must fit kSlots*(kPiece+2)*8 B.
-    static constexpr int kPieceFloats = kSlots * (kPiece + 2) * 2;
+    // consumed by then): KBW x kEpiStride floats must fit V::SLOTS*(V::PIECE+2)*8 B.
+    static constexpr int kPieceFloats = V::SLOTS * (V::PIECE + 2) * 2;
     // One epilogue pass covers 32 output channels (KL passes).
     static constexpr int kERraw = ((kPieceFloats / 32) - 1) / V::WO;
     static constexpr int kER = kERraw < 1 ? 1 : (kERraw > V::TY ? V::TY : kERraw);
     static constexpr int kEpiStride = (kER * V::WO) | 1;  // odd
     static_assert(32 * kEpiStride <= kPieceFloats, "epilogue buffer does not fit the piece slots");
     static constexpr size_t ring = sizeof(float) * V::STAGES * kStageFloats;
-    static constexpr size_t bars = 8 * (2 * V::STAGES + V::NW * kSlots);
+    static constexpr size_t bars = 8 * (2 * V::STAGES + V::NW * V::SLOTS);
     static constexpr size_t bars_pad = (bars + 127) / 128 * 128;
     // +2 entries: the interpreter prefetches one entry past EXIT, which for a
     // full piece in the last slot of the last warp lies beyond the ring
-    static constexpr size_t pieces = sizeof(uint2) * (V::NW * kSlots * (kPiece + 2) + 2);
+    static constexpr size_t pieces = sizeof(uint2) * (V::NW * V::SLOTS * (V::PIECE + 2) + 2);
     static constexpr size_t total = ring + bars_pad + pieces;
     static_assert(total * V::MINB <= 227 * 1024, "shared memory budget of the SM exceeded");
 };
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring);
     uint64_t* empty = full + STAGES;
-    uint64_t* pbar_all = empty + STAGES;  // [NW][kSlots]
+    uint64_t* pbar_all = empty + STAGES;  // [NW][V::SLOTS]
     uint2* piece_all = reinterpret_cast<uint2*>(smem + SM::ring + SM::bars_pad);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], (unsigned)nactive);
         }
-        for (int i = 0; i < NW * kSlots; ++i) mbar_init(&pbar_all[i], 1);
+        for (int i = 0; i < NW * V::SLOTS; ++i) mbar_init(&pbar_all[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     const int64_t stream = (int64_t)unit;  // = n * tiles + tile (ytiles == tiles)
     const uint2* sbase = a.entries + stream * a.cap;
     const uint32_t* of = a.offs + stream * (a.C + 1) + (int64_t)g * a.Cg;  // of[cl] = marker of channel g*Cg+cl
-    uint64_t* pbar = pbar_all + warp * kSlots;
-    uint2* pieces = piece_all + warp * kSlots * (kPiece + 2);
+    uint64_t* pbar = pbar_all + warp * V::SLOTS;
+    uint2* pieces = piece_all + warp * V::SLOTS * (V::PIECE + 2);
 
     // f32x2 bit patterns (low word = first element): channel pairs (KL >= 2) or
     // x pairs (KL == 1); odd KL adds one f32 accumulator per pixel
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         return q < 32 ? v0 : v1;
     };
     // Piece sequence: the range [bnd(0), bnd(nchunks)) cut at chunk
-    // boundaries and every kPiece entries.  Issue and consume cursors walk it
+    // boundaries and every V::PIECE entries.  Issue and consume cursors walk it
     // identically; lane 0 issues the bulk copies.
     int iq = 0;                 // issue cursor: chunk
     uint32_t ia = bnd(0);       // issue cursor: next entry
@@ -192,14 +192,14 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     int issued = 0;
     auto issue_next = [&]() {
         if (iq >= nchunks) return;
-        const uint32_t b = (ia + kPiece < iend) ? ia + kPiece : iend;
-        const int slot = issued % kSlots;
+        const uint32_t b = (ia + V::PIECE < iend) ? ia + V::PIECE : iend;
+        const int slot = issued % V::SLOTS;
         if (lane == 0) {
             const uint32_t a2 = ia & ~1u;
             const unsigned bytes = ((b - a2) * 8u + 15u) & ~15u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // EXIT write -> TMA overwrite
             mbar_expect_tx(&pbar[slot], bytes);
-            tma_bulk_g2s(pieces + slot * (kPiece + 2), sbase + a2, bytes, &pbar[slot]);
+            tma_bulk_g2s(pieces + slot * (V::PIECE + 2), sbase + a2, bytes, &pbar[slot]);
         }
         ++issued;
         ia = b;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         }
     };
 #pragma unroll 1
-    for (int i = 0; i < kSlots; ++i) issue_next();
+    for (int i = 0; i < V::SLOTS; ++i) issue_next();
 
     int consumed = 0;
     uint32_t ca = bnd(0);  // consume cursor
@@ -226,10 +226,10 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         mbar_wait(&full[st], (ch / STAGES) & 1);  // this chunk's weights have landed
 #pragma unroll 1
         while (ca < chunk_end) {
-            const uint32_t b = (ca + kPiece < chunk_end) ? ca + kPiece : chunk_end;
-            const int slot = consumed % kSlots;
-            mbar_wait(&pbar[slot], (consumed / kSlots) & 1);
-            uint2* p = pieces + slot * (kPiece + 2) + (ca & 1u);
+            const uint32_t b = (ca + V::PIECE < chunk_end) ? ca + V::PIECE : chunk_end;
+            const int slot = consumed % V::SLOTS;
+            mbar_wait(&pbar[slot], (consumed / V::SLOTS) & 1);
+            uint2* p = pieces + slot * (V::PIECE + 2) + (ca & 1u);
             if (lane == 0) p[b - ca] = make_uint2(0u, (unsigned)V::EXIT);
             __syncwarp();
             V::run(accp, accs, wp, ws, smem_u32(p), wlane, wlane_s, cbase);

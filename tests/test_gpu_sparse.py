@@ -269,7 +269,8 @@ def test_c5_chain_per_layer(sc):
         xd = out
 
 
-FORCED = [("C2", v) for v in (0, 1, 7, 10, 11, 12, 13)] + [("C4a", v) for v in (0, 2, 14)]
+FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28)] +
+          [("C4b", v) for v in (0, 4, 29, 30)])
 
 
 @pytest.mark.parametrize("cfg,variant", FORCED)

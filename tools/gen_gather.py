@@ -49,6 +49,12 @@ VARIANTS = [
     (12, "r3s3p1_w13_ty2_kl4_nw11", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3),  # C2: k-quads, 3 warps/SMSP
     (13, "r3s3p1_w13_ty5_kl2_nw11", 3, 3, 1, 13, 5, 2, 11, 1, 8, 4),  # C2: k-pairs, 3 warps/SMSP
     (14, "r3s3p1_w28_ty1_kl4_nw11", 3, 3, 1, 28, 1, 4, 11, 1, 8, 3),  # C4a: k-quads
+    # V12 with 16-channel weight chunks in a 2-stage ring: half the chunk boundaries (pieces, barrier
+    # handshakes); measured best of the CH/STAGES/SLOTS/PIECE sweep
+    (21, "r3s3p1_w13_ty2_kl4_nw11_ch16s2", 3, 3, 1, 13, 2, 4, 11, 1, 16, 2),
+    (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a
+    (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
+    (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),        # C4b
 ]
 
 # ablations of V12 for timing studies only (wrong results: never selected unless forced)
@@ -58,10 +64,10 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [12, 11, 10, 13, 7, 1, 14, 2]
+PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4]
 
 
-def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None):
+def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254):
     WO = W + 2 * P - S + 1
     XPAIR = KL == 1
     NX = (WO + 1) // 2 if XPAIR else WO            # accumulator columns per row
@@ -205,7 +211,8 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
     lines.append(f"struct V{vid} {{")
     for k, v in (("R", R), ("S", S), ("P", P), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
                  ("NW", NW), ("MINB", MINB), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
-                 ("NPAIR", NPAIR), ("NSING", NSING), ("NWP", len(wp)), ("NWS", max(1, len(ws)))):
+                 ("NPAIR", NPAIR), ("NSING", NSING), ("NWP", len(wp)), ("NWS", max(1, len(ws))),
+                 ("SLOTS", SLOTS), ("PIECE", PIECE)):
         lines.append(f"    static constexpr int {k} = {v};")
     lines.append(f"    static constexpr bool XPAIR = {'true' if XPAIR else 'false'};")
     lines.append(f'    static constexpr const char* NAME = "{name}";')
