@@ -253,8 +253,14 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     uint32_t total = 0;
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u) {
-        bal[u] = __ballot_sync(0xffffffffu, v[u] != 0.0f);  // IEEE: -0.0 is zero
-        if (v[u] != 0.0f) lst[total + __popc(bal[u] & lt)] = make_uint2(__float_as_uint(v[u]), 32u * u + lane);
+        const bool nz = v[u] != 0.0f;  // IEEE: -0.0 is zero
+        bal[u] = __ballot_sync(0xffffffffu, nz);
+        // predicated store (no branch / reconvergence per slot)
+        const uint2* dst = lst + total + __popc(bal[u] & lt);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.global.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(dst),
+            "r"(__float_as_uint(v[u])), "r"(32u * u + lane), "r"((unsigned)nz)
+            : "memory");
         total += __popc(bal[u]);
     }
     // lane r <= H: nonzeros before element r*W (the first element of row r)
@@ -391,12 +397,20 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     const int TYT = (int)(g.ty * g.T);
     const int planes = (int)(n * g.C);
     const unsigned cgrid = (unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps);
-    if (g.H * g.W <= 256)
-        compact_plane_count_kernel<8><<<cgrid, kPlaneWarps * 32, 0, st>>>(
-            in, planes, (int)g.C, (int)g.H, (int)g.W, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt, plist, prow);
-    else
-        compact_plane_count_kernel<kMaxSlots><<<cgrid, kPlaneWarps * 32, 0, st>>>(
-            in, planes, (int)g.C, (int)g.H, (int)g.W, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt, plist, prow);
+    // the smallest instantiated slot count covering the plane (loads of 32 elements)
+    const int64_t slots = (g.H * g.W + 31) / 32;
+#define SC_COUNT(NS)                                                                                             \
+    compact_plane_count_kernel<NS><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, planes, (int)g.C, (int)g.H, (int)g.W, \
+                                                                       TYT, (int)g.P, (int)g.nwr, (int)g.tiles,   \
+                                                                       cnt, plist, prow)
+    if (slots <= 2) SC_COUNT(2);
+    else if (slots <= 4) SC_COUNT(4);
+    else if (slots <= 6) SC_COUNT(6);
+    else if (slots <= 8) SC_COUNT(8);
+    else if (slots <= 16) SC_COUNT(16);
+    else if (slots <= 25) SC_COUNT(25);
+    else SC_COUNT(kMaxSlots);
+#undef SC_COUNT
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
