@@ -94,9 +94,9 @@ struct Smem {
     static constexpr size_t ring = sizeof(float) * V::STAGES * kStageFloats;
     static constexpr size_t bars = 8 * (2 * V::STAGES + V::NW * V::SLOTS);
     static constexpr size_t bars_pad = (bars + 127) / 128 * 128;
-    // +2 entries: the interpreter prefetches one entry past EXIT, which for a
+    // +4 entries: the interpreter prefetches up to two entries past EXIT, which for a
     // full piece in the last slot of the last warp lies beyond the ring
-    static constexpr size_t pieces = sizeof(uint2) * (V::NW * V::SLOTS * (V::PIECE + 2) + 2);
+    static constexpr size_t pieces = sizeof(uint2) * (V::NW * V::SLOTS * (V::PIECE + 2) + 4);
     static constexpr size_t total = ring + bars_pad + pieces;
     static_assert(total * V::MINB <= 227 * 1024, "shared memory budget of the SM exceeded");
 };

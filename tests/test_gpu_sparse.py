@@ -270,7 +270,7 @@ def test_c5_chain_per_layer(sc):
 
 
 FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28)] +
-          [("C4b", v) for v in (0, 4, 29, 30)])
+          [("C4b", v) for v in (0, 4, 29, 30)] + [("C3", v) for v in (0, 3, 33)])
 
 
 @pytest.mark.parametrize("cfg,variant", FORCED)
@@ -282,7 +282,7 @@ def test_forced_variants(sc, cfg, variant, s, monkeypatch):
     bit-exact on integer data."""
     monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
     shp = datagen.CONFIGS[cfg].with_batch(5)
-    x = datagen.activations(shp, s, seed=3)
+    x = datagen.activations(shp, "channel" if (cfg == "C3" and s > 0) else s, seed=3)
     w, b = datagen.weights(shp, seed=3)
     conv = make_conv(sc, shp, w, b, max_batch=9)
     assert conv.variant[0] == variant

@@ -54,6 +54,7 @@ VARIANTS = [
     (21, "r3s3p1_w13_ty2_kl4_nw11_ch16s2", 3, 3, 1, 13, 2, 4, 11, 1, 16, 2),
     (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a
     (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
+    (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
     (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),        # C4b
 ]
 
@@ -64,7 +65,7 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4]
+PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4, 33, 3]
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254):
@@ -161,13 +162,22 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
     NMASK = 1 << R
     LW, EXIT = NCASES, NCASES + NMASK
     chb = R * S * 32 * KL * 4   # bytes of one channel in the weight stage
-    asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
-           f"mov.b32 ep, %{pop};",
-           "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
-           "LOOP_%=:",
-           "mov.b32 xc, xn;", "mov.b32 cc, cn;",
-           "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
-           "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
+    if ablate == "pf2":  # entries prefetched two dispatches ahead
+        asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, x2, c2, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
+               f"mov.b32 ep, %{pop};",
+               "ld.shared.v2.b32 {xn, cn}, [ep];", "ld.shared.v2.b32 {x2, c2}, [ep+8];", "add.u32 ep, ep, 16;",
+               "LOOP_%=:",
+               "mov.b32 xc, xn;", "mov.b32 cc, cn;", "mov.b32 xn, x2;", "mov.b32 cn, c2;",
+               "ld.shared.v2.b32 {x2, c2}, [ep];", "add.u32 ep, ep, 8;",
+               "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
+    else:
+        asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
+               f"mov.b32 ep, %{pop};",
+               "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
+               "LOOP_%=:",
+               "mov.b32 xc, xn;", "mov.b32 cc, cn;",
+               "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
+               "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
     labels = ([f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)] +
               [f"LW{m}_%=" if m else "LOOP_%=" for m in range(NMASK)] + ["END_%="])
     asm.append("TS_%=: .branchtargets " + ", ".join(labels) + ";")

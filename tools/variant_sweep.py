@@ -12,7 +12,7 @@ from paper_1704_07724_b200 import datagen, sparseconv as sc  # noqa: E402
 from tools.probe_run import dev_time_us  # noqa: E402
 
 cfg = sys.argv[1]
-sps = [float(x) for x in sys.argv[2].split(",")]
+sps = [x if x == "channel" else float(x) for x in sys.argv[2].split(",")]
 vids = [int(v) for v in sys.argv[3].split()]
 shp = datagen.CONFIGS[cfg]
 w, b = datagen.weights(shp)
