@@ -120,8 +120,12 @@ sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float *d_in, float 
                               sc_stream_t stream);
 
 /* Dense comparison path: implicit GEMM on tcgen05 tensor cores,
- * operands rounded to TF32 (cvt.rna), fp32 accumulation.  Same buffer and
- * stream contract as sparse_conv_forward. */
+ * operands rounded to TF32 (cvt.rna), fp32 accumulation.  Two launches: the
+ * input is transposed to a plan-owned channels-last TF32 copy, then every
+ * (tap, 32-channel block) of a tile of whole output rows is one 4-D TMA box
+ * (zero-filled padding).  Same buffer and stream contract as
+ * sparse_conv_forward.  SC_ERR_UNSUPPORTED when a tile of one output row does
+ * not fit a UMMA N <= 256 (W_out > 256) or a TMA box. */
 sc_status dense_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *d_out,
                              sc_stream_t stream);
 

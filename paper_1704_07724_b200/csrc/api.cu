@@ -20,7 +20,9 @@ struct sc_plan_s {
     Geometry g;
     DenseGeom dg;
     float* wpack = nullptr;    // [G][Kg_pad/kbw][Cg][R][S][kbw] (pack.cu)
-    float* wdense = nullptr;   // [G][m_pad][kdim_pad], TF32-rounded (dense path)
+    float* wdense = nullptr;   // dense path A operand [G][mtiles][kblocks][128x32], TF32, swizzled
+    float* nhwc = nullptr;     // dense path: channels-last TF32 copy of the input [N][H][W][Cp]
+    alignas(64) unsigned char bmap[128];  // dense path: TMA map of nhwc
     float* bias = nullptr;     // [K]
     uint2* entries = nullptr;  // stage-1 tile streams [N][tiles][cap] (+2 entries of slack)
     uint32_t* offs = nullptr;  // [N][tiles][C+1]
@@ -104,14 +106,14 @@ sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int
     g->Kg = p->k / p->groups;
     g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
     choose_kernel(g, variant, name);
-    dg->kdim = g->Cg * g->R * g->S;
-    dg->kdim_pad = (dg->kdim + 31) / 32 * 32;
-    dg->m_pad = (g->Kg + 127) / 128 * 128;
+    sc::dense_geometry(*g, dg);
     const int64_t in_e = g->N * g->C * g->H * g->W, out_e = g->N * g->K * g->Ho * g->Wo;
     const int64_t w_e = g->G * g->Cg * g->R * g->S * g->Kg_pad;
     const int64_t s_e = g->N * g->tiles * g->cap;  // 8-byte entries; indices are u32 inside a stream
-    const int64_t d_e = g->G * dg->m_pad * dg->kdim_pad;
-    if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || s_e > kMaxElems || d_e > kMaxElems)
+    const int64_t d_e = (int64_t)sc::dense_workspace_floats(*g, *dg);
+    const int64_t h_e = g->N * g->H * g->W * dg->cp;
+    if (in_e > kMaxElems || out_e > kMaxElems || w_e > kMaxElems || s_e > kMaxElems || d_e > kMaxElems ||
+        h_e > kMaxElems)
         return fail(SC_ERR_UNSUPPORTED, "a tensor has >= 2^31 elements");
     return SC_OK;
 }
@@ -149,6 +151,7 @@ struct DeviceGuard {
 void free_plan(sc_plan_s* p) {
     cudaFree(p->wpack);
     cudaFree(p->wdense);
+    cudaFree(p->nhwc);
     cudaFree(p->bias);
     cudaFree(p->entries);
     cudaFree(p->offs);
@@ -225,9 +228,11 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     const DenseGeom& dg = plan->dg;
     cudaError_t e;
     const size_t wbytes = sizeof(float) * g.G * g.Cg * g.R * g.S * g.Kg_pad;
-    const size_t dbytes = sizeof(float) * (g.G * dg.m_pad * dg.kdim_pad + 2 * dg.kdim_pad);
+    const size_t dbytes = sizeof(float) * sc::dense_workspace_floats(g, dg);
+    const size_t hbytes = sizeof(float) * g.N * g.H * g.W * dg.cp;
     if ((e = cudaMalloc(&plan->wpack, wbytes)) != cudaSuccess ||
         (e = cudaMalloc(&plan->wdense, dbytes)) != cudaSuccess ||
+        (dg.supported && (e = cudaMalloc(&plan->nhwc, hbytes)) != cudaSuccess) ||
         (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
         (e = cudaMalloc(&plan->entries, sizeof(uint2) * (g.N * g.tiles * g.cap + 2))) != cudaSuccess ||
         (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess ||
@@ -248,6 +253,7 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     if (e == cudaSuccess) e = cudaMemsetAsync(plan->entries, 0, sizeof(uint2) * (g.N * g.tiles * g.cap + 2), st0);
     if (e == cudaSuccess) e = sc::launch_pack_weights(g, d_weight, plan->wpack, st0);
     if (e == cudaSuccess) e = sc::launch_pack_dense(g, dg, d_weight, plan->wdense, st0);
+    if (e == cudaSuccess && dg.supported) e = sc::encode_dense_input_map(g, dg, plan->nhwc, plan->bmap);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st0);
     if (e != cudaSuccess) {
         free_plan(plan);
@@ -300,8 +306,8 @@ sc_status dense_conv_forward(sc_plan plan, int64_t n, const float* d_in, float* 
     if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
     if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
-    cudaError_t e = sc::launch_dense_tc(plan->g, plan->dg, n, d_in, plan->wdense, plan->bias, d_out,
-                                        (cudaStream_t)stream);
+    cudaError_t e = sc::launch_dense_tc(plan->g, plan->dg, n, d_in, plan->nhwc, plan->bmap, plan->wdense, plan->bias,
+                                        d_out, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) return fail(SC_ERR_UNSUPPORTED, "dense path: shape not supported");
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "dense launch");
 }
@@ -353,7 +359,7 @@ sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t* variant, const char*
 sc_status sparse_conv_launch_count(sc_plan plan, int32_t* sparse_launches, int32_t* dense_launches) {
     if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
     if (sparse_launches) *sparse_launches = sc::compact_uses_counts(plan->g) ? 3 : 2;
-    if (dense_launches) *dense_launches = 1;
+    if (dense_launches) *dense_launches = 2;
     return SC_OK;
 }
 

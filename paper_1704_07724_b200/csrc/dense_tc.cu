@@ -4,43 +4,46 @@
 //
 //   D[m][p] = sum_kk A[m][kk] * B[kk][p] + bias[m]
 //   m  = output channel within group g          (M_K rows, "matrix of kernels")
-//   kk = (cl, r, t) flattened = cl*R*S + r*S + t (the R*S*C axis of Fig. 2)
-//   p  = (n, y, x) flattened output pixel        (M_I columns; never materialised)
+//   kk = (r, t, cl) flattened, channels innermost (the R*S*C axis of Fig. 2)
+//   p  = output pixel (y, x) of one image        (M_I columns; never materialised)
 //   B[kk][p] = in[n][g*Cg + cl][y*T + r - P][x*T + t - P]  (0 outside: padding)
 //
-// Tiles: BM = 128 filters (UMMA M), BN = 128 pixels (UMMA N), BK = 32 (one
-// 128-byte swizzle row of TF32).  Operands are K-major, SWIZZLE_128B.
-//  * A: pre-packed at plan creation into the exact swizzled shared-memory image
-//    of every (g, m-tile, k-block) and rounded to TF32 (cvt.rna); one 16 KB
-//    1-D TMA bulk copy per stage (warp 9).
-//  * B: im2col on the fly by 8 producer warps: each thread owns one pixel row
-//    and four 16-byte chunks per stage, loads 16 input values (coalesced
-//    across the warp = consecutive pixels), rounds to TF32 (cvt.rna), stores
-//    swizzled with STS.128, fence.proxy.async, arrives on the stage's mbarrier.
-//  * MMA: warp 8, one thread: 4 x tcgen05.mma (K=8) per stage, tcgen05.commit
-//    frees the stage; the last commit signals the epilogue.
-//  * Epilogue: warps 0-3 read their 32 TMEM lanes (tcgen05.ld 32x32b.x32),
-//    transpose through shared memory and store pixel-contiguous runs + bias
-//    (+ optional ReLU, Eq. 2).
+// Two kernels per forward:
+//  1. nchw_to_nhwc: the input is transposed to channels-last and rounded to
+//     TF32 (cvt.rna) into a plan-owned buffer [N][H][W][Cp] (Cp = C rounded up
+//     to 4: 16-byte TMA strides), so that every (tap, 32-channel block) of a
+//     pixel tile is ONE 4-D TMA box: 32 channels x Wo columns x ROWS rows of one
+//     image, stride T in both spatial dimensions, zero-filled outside the image
+//     (that is the padding).  Each pixel row is 128 bytes = one SWIZZLE_128B
+//     line, i.e. exactly the K-major UMMA B tile.
+//  2. dense_tc: CTA = (image, tile of ROWS output rows, 128 filters, group).
+//     Warp 4 issues the TMA loads (A: a 16 KB 1-D bulk copy of the pre-packed,
+//     pre-swizzled, TF32-rounded weight block; B: the 4-D box), warp 5 one
+//     thread issues 4 x tcgen05.mma (K=8) per 32-channel block into a TMEM
+//     accumulator of N = ROWS*Wo (rounded up to 16) columns, and warps 0-3 read
+//     TMEM back (tcgen05.ld), transpose through shared memory and store NCHW
+//     runs + bias (+ optional ReLU, Eq. 2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "sc_internal.h"
 
 namespace sc {
 namespace dense {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 4;
-constexpr int kProducerWarps = 8, kMmaWarp = 8, kALoadWarp = 9, kThreads = 320;
-constexpr int kTileBytes = BM * BK * 4;  // 16 KB for A and for B
-constexpr uint32_t kTmemCols = 128;
+constexpr int BM = 128, BK = 32, STAGES = 4;
+constexpr int kEpiWarps = 4, kTmaWarp = 4, kMmaWarp = 5, kThreads = 192;
+constexpr int kATileBytes = BM * BK * 4;  // 16 KB
+constexpr int kBTileBytes = 256 * BK * 4; // up to 256 pixel rows of 128 B
+constexpr uint32_t kTmemCols = 256;
 
 struct Args {
-    const float* in;
     const float* adense;  // [G][mtiles][kblocks][128*32] swizzled TF32 image
-    const int2* ktab;     // [kblocks*32]: (cl*H*W + r*W + t, r<<16 | t), r = 0x7fff for padding kk
     const float* bias;
     float* out;
-    int C, H, W, K, Kg, Cg, T, P, Ho, Wo, HoWo, relu;
-    int mtiles, ntiles, kblocks;
-    long long ptotal;
+    int K, Kg, Cg, R, S, T, P, Ho, Wo, HoWo, relu;
+    int rows, ptiles, mtiles, cb, kblocks, npix, nmma;
+    uint32_t idesc;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -48,9 +51,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
@@ -70,6 +70,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c, int x, int y, int n,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(y), "r"(n), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ float to_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -82,33 +90,53 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
            ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
-// Instruction descriptor: D f32 [4,6)=1, A tf32 [7,10)=2, B tf32 [10,13)=2,
-// both K-major, N>>3 at [17,23), M>>4 at [24,29).
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
 
-__global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
+// in [N][C][H*W] -> nhwc [N][H*W][Cp], TF32-rounded (RNA); channels >= C are 0.
+__global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                          int C, int Cp, int HW) {
+    __shared__ float tile[32][33];
+    const int n = blockIdx.z;
+    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const float* src = in + (size_t)n * C * HW;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int c = c0 + ty + i, p = p0 + tx;
+        tile[ty + i][tx] = (c < C && p < HW) ? to_tf32(__ldg(src + (size_t)c * HW + p)) : 0.f;
+    }
+    __syncthreads();
+    float* dst = out + (size_t)n * HW * Cp;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int p = p0 + ty + i, c = c0 + tx;
+        if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][ty + i];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ CUtensorMap bmap, const Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the swizzle atoms
-    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    float* sA = reinterpret_cast<float*>(smem);                          // STAGES x 16 KB
-    float* sB = reinterpret_cast<float*>(smem + STAGES * kTileBytes);    // STAGES x 16 KB
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * kTileBytes);
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128 atoms
+    unsigned char* sA = smem;                                  // STAGES x 16 KB
+    unsigned char* sB = smem + STAGES * kATileBytes;           // STAGES x 32 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kBTileBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-    float* epi = reinterpret_cast<float*>(smem + 2 * STAGES * kTileBytes + 256);  // 4 warps x 32 x 33
+    float* epi = reinterpret_cast<float*>(sB + STAGES * kBTileBytes + 256);  // 4 warps x 32 x 33
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int bid = blockIdx.x;
-    const int nt = bid % a.ntiles;
-    bid /= a.ntiles;
+    const int pt = bid % a.ptiles;
+    bid /= a.ptiles;
     const int mt = bid % a.mtiles;
-    const int g = bid / a.mtiles;
+    bid /= a.mtiles;
+    const int g = bid % (a.K / a.Kg);
+    const int n = bid / (a.K / a.Kg);
+    const int y0 = pt * a.rows;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], kProducerWarps + 1);
+            mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
@@ -126,52 +154,19 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
     const uint32_t tmem = *tmem_slot;
     const int nk = a.kblocks;
 
-    if (warp < kProducerWarps) {
-        // ---- B producers: one pixel row per thread, chunks {c0, c0+2, c0+4, c0+6} ----
-        const int t = threadIdx.x;
-        const int row = t & (BN - 1);
-        const int c0 = t >> 7;  // 0 or 1
-        const long long p = (long long)nt * BN + row;
-        const bool pvalid = p < a.ptotal;
-        int n = 0, y = 0, x = 0;
-        if (pvalid) {
-            n = (int)(p / a.HoWo);
-            const int pix = (int)(p - (long long)n * a.HoWo);
-            y = pix / a.Wo;
-            x = pix - y * a.Wo;
-        }
-        const int yb = y * a.T - a.P, xb = x * a.T - a.P;
-        const float* pin = a.in + ((long long)n * a.C + (long long)g * a.Cg) * a.H * a.W + (long long)yb * a.W + xb;
-        const int swz = row & 7;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-            float* dst = sB + s * (kTileBytes / 4) + row * BK;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int ch = c0 + 2 * i;
-                float v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int2 e = __ldg(&a.ktab[kb * BK + ch * 4 + q]);
-                    const int r = e.y >> 16, tt = e.y & 0xffff;
-                    const bool ok = pvalid && (unsigned)(yb + r) < (unsigned)a.H && (unsigned)(xb + tt) < (unsigned)a.W;
-                    v[q] = ok ? to_tf32(__ldg(pin + e.x)) : 0.f;
-                }
-                *reinterpret_cast<float4*>(dst + ((ch ^ swz) << 2)) = make_float4(v[0], v[1], v[2], v[3]);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
-        }
-    } else if (warp == kALoadWarp) {
+    if (warp == kTmaWarp) {
         if (lane == 0) {
-            const float* asrc = a.adense + ((long long)g * a.mtiles + mt) * nk * (kTileBytes / 4);
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+            const float* asrc = a.adense + ((size_t)g * a.mtiles + mt) * nk * (kATileBytes / 4);
+            const unsigned bbytes = (unsigned)(a.npix * BK * 4);
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                mbar_expect_tx(&full[s], kTileBytes);
-                tma_bulk_g2s(sA + s * (kTileBytes / 4), asrc + (long long)kb * (kTileBytes / 4), kTileBytes, &full[s]);
+                if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+                const int rs = kb / a.cb, cb = kb - rs * a.cb;
+                const int r = rs / a.S, t = rs - r * a.S;
+                mbar_expect_tx(&full[s], kATileBytes + bbytes);
+                tma_bulk_g2s(sA + s * kATileBytes, asrc + (size_t)kb * (kATileBytes / 4), kATileBytes, &full[s]);
+                tma_load_4d(sB + s * kBTileBytes, &bmap, g * a.Cg + cb * BK, t - a.P, y0 * a.T + r - a.P, n, &full[s]);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -180,8 +175,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
             mbar_wait(&full[s], (kb / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
-                const uint32_t abase = smem_u32(sA + s * (kTileBytes / 4));
-                const uint32_t bbase = smem_u32(sB + s * (kTileBytes / 4));
+                const uint32_t abase = smem_u32(sA + s * kATileBytes);
+                const uint32_t bbase = smem_u32(sB + s * kBTileBytes);
 #pragma unroll
                 for (int k = 0; k < BK / 8; ++k) {
                     const uint64_t ad = sw128_desc(abase + k * 32);
@@ -191,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
                         "{\n\t.reg .pred p;\n\t"
                         "setp.ne.b32 p, %4, 0;\n\t"
                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                        "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc)
+                        "l"(ad), "l"(bd), "r"(a.idesc), "r"(acc)
                         : "memory");
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -205,15 +200,15 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
                              smem_u32(tmem_full))
                          : "memory");
         __syncwarp();
-    }
-
-    // ---- epilogue: warps 0-3 own TMEM lanes 32w..32w+31 (= output channels) ----
-    if (warp < 4) {
+    } else {
+        // ---- epilogue: warps 0-3 own TMEM lanes 32w..32w+31 (= output channels) ----
         mbar_wait(tmem_full, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float* buf = epi + warp * 32 * 33;
         const int m0 = mt * BM + warp * 32;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        int valid = a.HoWo - y0 * a.Wo;  // pixels of this tile inside the image
+        if (valid > a.npix) valid = a.npix;
+        for (int c0 = 0; c0 < a.nmma; c0 += 32) {
             uint32_t r[32];
             const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
             asm volatile(
@@ -229,18 +224,16 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(r[j]);  // [m][pixel]
             __syncwarp();
-            const long long p = (long long)nt * BN + c0 + lane;
-            if (p < a.ptotal) {
-                const int n = (int)(p / a.HoWo);
-                const int pix = (int)(p - (long long)n * a.HoWo);
-                float* dst = a.out + ((long long)n * a.K + (long long)g * a.Kg) * a.HoWo + pix;
+            const int pix = c0 + lane;
+            if (pix < valid) {
+                float* dst = a.out + ((size_t)n * a.K + (size_t)g * a.Kg) * a.HoWo + (size_t)y0 * a.Wo + pix;
 #pragma unroll 4
                 for (int mm = 0; mm < 32; ++mm) {
                     const int m = m0 + mm;
                     if (m < a.Kg) {
                         float o = buf[mm * 33 + lane] + __ldg(&a.bias[g * a.Kg + m]);
                         if (a.relu) o = fmaxf(o, 0.f);
-                        dst[(long long)m * a.HoWo] = o;
+                        dst[(size_t)m * a.HoWo] = o;
                     }
                 }
             }
@@ -255,11 +248,13 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const Args a) {
     }
 }
 
-// Pack A: adense[g][mt][kb][row][32] in the K-major SWIZZLE_128B image:
-// element (row, k) at row*32 + ((k/4) ^ (row%8))*4 + k%4, value
-// tf32_rna(W[g*Kg + mt*128 + row][kk = kb*32 + k]) or 0 outside.
-__global__ void pack_dense_kernel(const float* __restrict__ w, float* __restrict__ adense, int2* __restrict__ ktab,
-                                  int G, int Kg, int mtiles, int kblocks, int kdim, int RS, int S, int H, int W) {
+// Pack A: adense[g][mt][kb][row][32] in the K-major SWIZZLE_128B image, kb =
+// (r*S + t)*cb + channel block: element (row, k) at row*32 + ((k/4) ^ (row%8))*4
+// + k%4 holds tf32_rna(W[g*Kg + mt*128 + row][cl = cblock*32 + k][r][t]), 0
+// outside (m >= Kg or cl >= Cg).
+__global__ void pack_dense_kernel(const float* __restrict__ w, float* __restrict__ adense, int G, int Kg, int Cg,
+                                  int RS, int mtiles, int cb) {
+    const int kblocks = RS * cb;
     const long long total = (long long)G * mtiles * kblocks * BM * BK;
     for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
          o += (long long)gridDim.x * blockDim.x) {
@@ -272,59 +267,102 @@ __global__ void pack_dense_kernel(const float* __restrict__ w, float* __restrict
         const int row = within / BK, slot = within % BK;
         const int chunk = (slot >> 2) ^ (row & 7);  // stored chunk -> logical chunk
         const int k = chunk * 4 + (slot & 3);
-        const int m = mt * BM + row, kk = kb * BK + k;
+        const int rs = kb / cb, cl = (kb - rs * cb) * BK + k;
+        const int m = mt * BM + row;
         float v = 0.f;
-        if (m < Kg && kk < kdim) v = to_tf32(w[((long long)g * Kg + m) * kdim + kk]);
+        if (m < Kg && cl < Cg) v = to_tf32(w[(((long long)g * Kg + m) * Cg + cl) * RS + rs]);
         adense[o] = v;
     }
-    // im2col gather table (index metadata, same for every group)
-    for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < kblocks * BK; kk += gridDim.x * blockDim.x) {
-        if (kk < kdim) {
-            const int cl = kk / RS, rs = kk - cl * RS, r = rs / S, t = rs - r * S;
-            ktab[kk] = make_int2(cl * H * W + r * W + t, (r << 16) | t);
-        } else {
-            ktab[kk] = make_int2(0, 0x7fff << 16);
-        }
+}
+
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+
+EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
     }
+    return fn;
 }
 
 }  // namespace dense
 
-cudaError_t launch_pack_dense(const Geometry& g, const DenseGeom& dg, const float* w, float* wdense,
-                              cudaStream_t st) {
+// Tile geometry of the dense path (plan creation).  supported = false when a
+// pixel tile of whole output rows cannot fit one UMMA N <= 256 or a TMA box.
+void dense_geometry(const Geometry& g, DenseGeom* dg) {
     using namespace dense;
-    const int mtiles = (int)(dg.m_pad / BM), kblocks = (int)(dg.kdim_pad / BK);
-    int2* ktab = reinterpret_cast<int2*>(wdense + g.G * dg.m_pad * dg.kdim_pad);
-    pack_dense_kernel<<<512, 256, 0, st>>>(w, wdense, ktab, (int)g.G, (int)g.Kg, mtiles, kblocks, (int)dg.kdim,
-                                            (int)(g.R * g.S), (int)g.S, (int)g.H, (int)g.W);
-    return cudaGetLastError();
+    dg->cp = (g.C + 3) / 4 * 4;
+    dg->cb = (g.Cg + BK - 1) / BK;
+    dg->kblocks = g.R * g.S * dg->cb;
+    dg->mtiles = (g.Kg + BM - 1) / BM;
+    int64_t rows = 256 / g.Wo;
+    if (rows > g.Ho) rows = g.Ho;
+    dg->rows = rows;
+    dg->ptiles = rows > 0 ? (g.Ho + rows - 1) / rows : 0;
+    dg->npix = rows * g.Wo;
+    dg->nmma = (dg->npix + 15) / 16 * 16;
+    dg->supported = rows >= 1 && g.Wo * g.T <= 256 && rows * g.T <= 256 && dg->nmma <= 256 && dg->nmma >= 16;
 }
 
 size_t dense_workspace_floats(const Geometry& g, const DenseGeom& dg) {
-    return (size_t)(g.G * dg.m_pad * dg.kdim_pad + 2 * dg.kdim_pad);
+    return (size_t)(g.G * dg.mtiles * dg.kblocks * dense::BM * dense::BK);
 }
 
-cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, const float* wdense,
-                            const float* bias, float* out, cudaStream_t st) {
+cudaError_t launch_pack_dense(const Geometry& g, const DenseGeom& dg, const float* w, float* wdense,
+                              cudaStream_t st) {
     using namespace dense;
+    pack_dense_kernel<<<512, 256, 0, st>>>(w, wdense, (int)g.G, (int)g.Kg, (int)g.Cg, (int)(g.R * g.S),
+                                            (int)dg.mtiles, (int)dg.cb);
+    return cudaGetLastError();
+}
+
+cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float* nhwc, void* map128) {
+    using namespace dense;
+    EncodeTiled enc = encoder();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[4] = {(cuuint64_t)dg.cp, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    const cuuint64_t strides[3] = {(cuuint64_t)dg.cp * 4, (cuuint64_t)(dg.cp * g.W * 4),
+                                   (cuuint64_t)(dg.cp * g.W * g.H * 4)};
+    const cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)(g.Wo * g.T), (cuuint32_t)(dg.rows * g.T), 1};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)g.T, (cuuint32_t)g.T, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, nhwc, dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, float* nhwc,
+                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st) {
+    using namespace dense;
+    if (!dg.supported) return cudaErrorNotSupported;
+    const int HW = (int)(g.H * g.W);
+    dim3 tgrid((unsigned)((HW + 31) / 32), (unsigned)((dg.cp + 31) / 32), (unsigned)n);
+    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, HW);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     Args a;
-    a.in = in;
     a.adense = wdense;
-    a.ktab = reinterpret_cast<const int2*>(wdense + g.G * dg.m_pad * dg.kdim_pad);
     a.bias = bias;
     a.out = out;
-    a.C = (int)g.C; a.H = (int)g.H; a.W = (int)g.W; a.K = (int)g.K; a.Kg = (int)g.Kg; a.Cg = (int)g.Cg;
+    a.K = (int)g.K; a.Kg = (int)g.Kg; a.Cg = (int)g.Cg; a.R = (int)g.R; a.S = (int)g.S;
     a.T = (int)g.T; a.P = (int)g.P; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo; a.HoWo = (int)(g.Ho * g.Wo);
     a.relu = g.relu ? 1 : 0;
-    a.mtiles = (int)(dg.m_pad / BM);
-    a.kblocks = (int)(dg.kdim_pad / BK);
-    a.ptotal = (long long)n * g.Ho * g.Wo;
-    a.ntiles = (int)((a.ptotal + BN - 1) / BN);
-    const size_t smem = 1024 + 2 * STAGES * kTileBytes + 256 + 4 * 32 * 33 * 4;
-    cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    a.rows = (int)dg.rows; a.ptiles = (int)dg.ptiles; a.mtiles = (int)dg.mtiles; a.cb = (int)dg.cb;
+    a.kblocks = (int)dg.kblocks; a.npix = (int)dg.npix; a.nmma = (int)dg.nmma;
+    // instruction descriptor: D f32 [4,6)=1, A tf32 [7,10)=2, B tf32 [10,13)=2, both K-major,
+    // N>>3 at [17,23), M>>4 at [24,29)
+    a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(dg.nmma >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    const size_t smem = 1024 + STAGES * (kATileBytes + kBTileBytes) + 256 + kEpiWarps * 32 * 33 * 4;
+    e = cudaFuncSetAttribute(dense_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long long grid = (long long)a.ntiles * a.mtiles * g.G;
-    dense_tc_kernel<<<(unsigned)grid, kThreads, smem, st>>>(a);
+    const long long grid = (long long)n * g.G * dg.mtiles * dg.ptiles;
+    CUtensorMap map;
+    memcpy(&map, map128, sizeof(map));
+    dense_tc_kernel<<<(unsigned)grid, kThreads, smem, st>>>(map, a);
     return cudaGetLastError();
 }
 

@@ -22,17 +22,22 @@ struct Geometry {
     bool relu;
 };
 
-// Dense tcgen05 path operand geometry.
+// Dense tcgen05 path geometry (dense_tc.cu): channels-last input with Cp = C
+// rounded up to 4; K-dim blocks of 32 channels per tap (cb per group); tiles
+// of `rows` whole output rows (npix = rows*Wo pixels, UMMA N = nmma).
 struct DenseGeom {
-    int64_t kdim;        // Cg*R*S
-    int64_t kdim_pad;    // rounded up to 32 (one 128-byte TF32 row)
-    int64_t m_pad;       // Kg rounded up to 128 (UMMA M)
+    int64_t cp, cb, kblocks, mtiles, rows, ptiles, npix, nmma;
+    bool supported;
 };
 
 // ---- kernels (launchers return cudaGetLastError()) -------------------------
 cudaError_t launch_pack_weights(const Geometry& g, const float* w, float* wpack, cudaStream_t st);
+void dense_geometry(const Geometry& g, DenseGeom* dg);
+size_t dense_workspace_floats(const Geometry& g, const DenseGeom& dg);  // packed A
 cudaError_t launch_pack_dense(const Geometry& g, const DenseGeom& dg, const float* w, float* wdense,
                               cudaStream_t st);
+// Encode the 4-D TMA map (128 bytes) of the plan's NHWC input buffer.
+cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float* nhwc, void* map128);
 // Stage 1.  The plane-major path (compact_uses_counts) needs workspaces
 // cnt [N][tiles][C] u32, plist [N*C][H*W] (bits, index) pairs and
 // prow [N*C][H+1] u32; they may be null otherwise.
@@ -51,8 +56,8 @@ cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const 
                                cudaStream_t st);
 
 // Dense tcgen05 TF32 implicit GEMM (dense_tc.cu).
-cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in,
-                            const float* wdense, const float* bias, float* out, cudaStream_t st);
+cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, float* nhwc,
+                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st);
 
 cudaError_t probe_fma(int kind, double* rate);
 cudaError_t launch_flush(void* scratch, size_t bytes, cudaStream_t st);
