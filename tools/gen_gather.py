@@ -171,15 +171,23 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
                "ld.shared.v2.b32 {x2, c2}, [ep];", "add.u32 ep, ep, 8;",
                "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
     else:
-        asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es;", ".reg .f32 al, ah, wl, wh, vf;",
+        asm = ["{", ".reg .b64 vv;", ".reg .b32 xc, cc, xn, cn, ep, ea, es, mk, mr;", ".reg .pred pm, pr;",
+               ".reg .f32 al, ah, wl, wh, vf;",
                f"mov.b32 ep, %{pop};",
                "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
                "LOOP_%=:",
                "mov.b32 xc, xn;", "mov.b32 cc, cn;",
                "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
                "mov.b64 vv, {xc, xc};", "mov.b32 vf, xc;"]
-    labels = ([f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)] +
-              [f"LW{m}_%=" if m else "LOOP_%=" for m in range(NMASK)] + ["END_%="])
+    if ablate == "inline":
+        # markers (code >= LOADW) leave through a direct branch before the jump table;
+        # only nonzero entries pay the LDC + BRX dispatch
+        asm.append(f"setp.ge.u32 pm, cc, {LW};")
+        asm.append("@pm bra.uni MK_%=;")
+        labels = [f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)]
+    else:
+        labels = ([f"C{i}_%=" if b else "LOOP_%=" for i, b in enumerate(bodies)] +
+                  [f"LW{m}_%=" if m else "LOOP_%=" for m in range(NMASK)] + ["END_%="])
     asm.append("TS_%=: .branchtargets " + ", ".join(labels) + ";")
     asm.append("brx.idx.uni cc, TS_%=;")
     for i, b in enumerate(bodies):
@@ -188,7 +196,38 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
             asm += b
             asm.append("bra.uni LOOP_%=;")
     tap_bytes = 32 * KL * 4
-    for m in range(1, NMASK):
+    if ablate == "inline":
+        # marker: EXIT leaves; otherwise mask = code - LOADW, weights of the masked filter
+        # rows loaded with row-predicated shared loads (no jump table)
+        asm.append("MK_%=:")
+        asm.append(f"setp.ge.u32 pm, cc, {EXIT};")
+        asm.append("@pm bra.uni END_%=;")
+        asm.append(f"sub.u32 mk, cc, {LW};")
+        asm.append(f"sub.u32 ea, xc, %{cbop};")
+        if NSING:
+            asm.append(f"mad.lo.u32 es, ea, {chb}, %{wsop};")
+        asm.append(f"mad.lo.u32 ea, ea, {chb}, %{wlop};")
+        for r in range(R):
+            asm.append(f"and.b32 mr, mk, {1 << r};")
+            asm.append("setp.ne.u32 pr, mr, 0;")
+            for i, key in enumerate(wkeys):
+                if key[0] != r:
+                    continue
+                if XPAIR:
+                    pass
+                elif NPAIR == 1:
+                    asm.append(f"@pr ld.shared.b64 %{wp[(key, 0)]}, [ea+{i * tap_bytes}];")
+                else:
+                    asm.append(f"@pr ld.shared.v2.b64 {{%{wp[(key, 0)]}, %{wp[(key, 1)]}}}, [ea+{i * tap_bytes}];")
+                if NSING:
+                    asm.append(f"@pr ld.shared.f32 %{ws[key]}, [es+{i * tap_bytes + 256}];")
+            if XPAIR:
+                for u in range(1, S):
+                    asm.append(f"@pr ld.shared.f32 wl, [ea+{(r * S + u) * 128}];")
+                    asm.append(f"@pr ld.shared.f32 wh, [ea+{(r * S + u - 1) * 128}];")
+                    asm.append(f"@pr mov.b64 %{wp[((r, u), 0)]}, {{wl, wh}};")
+        asm.append("bra.uni LOOP_%=;")
+    for m in range(1, NMASK if ablate != "inline" else 1):
         asm.append(f"LW{m}_%=:")
         asm.append(f"sub.u32 ea, xc, %{cbop};")
         if NSING:
