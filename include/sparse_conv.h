@@ -136,6 +136,22 @@ sc_status dense_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *
 sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, float *h_out,
                                    sc_stream_t stream);
 
+/* A chain of layers (e.g. C5: conv3 -> ReLU -> conv4 -> ReLU -> conv5, the
+ * ReLUs fused via SC_FLAG_FUSE_RELU) on the first n images: plans[l+1]'s input
+ * is plans[l]'s output (K, H_out, W_out must match C, H, W).  d_in is layer
+ * 0's NCHW input; d_outs[l] is layer l's NCHW output buffer (caller-owned).
+ * d_outs[nplans-1] is required; an intermediate d_outs[l] may be NULL, in
+ * which case layer l writes no dense output and instead emits layer l+1's
+ * stage-1 input directly from its epilogue (ISC step 1 fused into the
+ * producer: "eliminates the unused zero operands on-the-fly", P:29, P:33;
+ * SURVEY 8f row f1): per-(plane, row) nonzero lists that layer l+1's stage 1
+ * turns into the same R9 streams without re-reading a dense tensor.  Returns
+ * SC_ERR_UNSUPPORTED if such an intermediate layer cannot emit lists (its
+ * stage-2 kernel is the generic one or a KL=1 variant) and d_outs[l] is NULL.
+ * Stream-ordered, asynchronous, graph-capturable like sparse_conv_forward. */
+sc_status sparse_conv_forward_chain(const sc_plan *plans, int32_t nplans, int64_t n, const float *d_in,
+                                    float *const *d_outs, sc_stream_t stream);
+
 /* Free everything the plan owns.  NULL is a no-op. */
 sc_status sparse_conv_destroy(sc_plan plan);
 

@@ -287,7 +287,7 @@ sc_status sparse_conv_gather(sc_plan plan, int64_t n, float* d_out, sc_stream_t 
     cudaError_t e;
     if (plan->variant > 0)
         e = sc::launch_gather_fast(plan->variant, plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias,
-                                   d_out, (cudaStream_t)stream);
+                                   d_out, nullptr, nullptr, (cudaStream_t)stream);
     else
         e = sc::launch_gather_generic(plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias, d_out,
                                       (cudaStream_t)stream);
@@ -332,6 +332,59 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
     if ((e = cudaMemcpyAsync(h_out, plan->stage_out, nout, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return cuda_fail(e, "D2H copy");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+    return SC_OK;
+}
+
+sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_t n, const float* d_in,
+                                   float* const* d_outs, sc_stream_t stream) {
+    if (!plans || nplans < 1 || !d_outs) return fail(SC_ERR_INVALID_ARGUMENT, "bad chain arguments");
+    for (int l = 0; l < nplans; ++l) {
+        sc_status st = check_forward(plans[l], n);
+        if (st != SC_OK) return st;
+        if (l > 0 && plans[l]->device != plans[0]->device)
+            return fail(SC_ERR_INVALID_ARGUMENT, "chain plans live on different devices");
+        if (l + 1 < nplans) {
+            const Geometry &a = plans[l]->g, &b = plans[l + 1]->g;
+            if (a.K != b.C || a.Ho != b.H || a.Wo != b.W)
+                return fail(SC_ERR_SHAPE, "layer %d output %lldx%lldx%lld does not match layer %d input", l,
+                            (long long)a.K, (long long)a.Ho, (long long)a.Wo, l + 1);
+        }
+    }
+    sc_status st = check_dev_ptr(plans[0], d_in, "d_in");
+    if (st != SC_OK) return st;
+    if ((st = check_dev_ptr(plans[0], d_outs[nplans - 1], "d_outs[last]")) != SC_OK) return st;
+    for (int l = 0; l + 1 < nplans; ++l)
+        if (d_outs[l] && (st = check_dev_ptr(plans[0], d_outs[l], "d_outs[l]")) != SC_OK) return st;
+    DeviceGuard guard(plans[0]->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    bool lists_ready = false;  // plans[l]'s row lists were written by layer l-1's gather
+    for (int l = 0; l < nplans; ++l) {
+        sc_plan_s* p = plans[l];
+        cudaError_t e;
+        if (l == 0) {
+            e = sc::launch_compact(p->g, n, d_in, p->cnt, p->plist, p->prow, p->entries, p->offs, s);
+        } else if (lists_ready) {
+            e = sc::launch_compact_from_rows(p->g, n, p->cnt, p->plist, p->prow, p->entries, p->offs, s);
+        } else {
+            if (!d_outs[l - 1])
+                return fail(SC_ERR_UNSUPPORTED, "layer %d cannot emit chained lists: d_outs[%d] is required", l - 1,
+                            l - 1);
+            e = sc::launch_compact(p->g, n, d_outs[l - 1], p->cnt, p->plist, p->prow, p->entries, p->offs, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "chain stage 1");
+        sc_plan_s* next = l + 1 < nplans ? plans[l + 1] : nullptr;
+        const bool emit = next && p->variant > 0 && sc::gather_fast_can_emit(p->variant) &&
+                          sc::compact_uses_counts(next->g) && next->plist && next->prow;
+        float* out = d_outs[l];
+        if (!emit && !out) return fail(SC_ERR_UNSUPPORTED, "layer %d needs an output buffer (no list emission)", l);
+        if (p->variant > 0)
+            e = sc::launch_gather_fast(p->variant, p->g, n, p->entries, p->offs, p->wpack, p->bias, out,
+                                       emit ? next->plist : nullptr, emit ? next->prow : nullptr, s);
+        else
+            e = sc::launch_gather_generic(p->g, n, p->entries, p->offs, p->wpack, p->bias, out, s);
+        if (e != cudaSuccess) return cuda_fail(e, "chain gather");
+        lists_ready = emit;
+    }
     return SC_OK;
 }
 

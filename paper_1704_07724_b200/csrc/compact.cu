@@ -280,11 +280,17 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     if (lane < tiles) cnt[((int64_t)n * tiles + lane) * C + c] = r1 > r0 ? p1 - p0 : 0u;
 }
 
+// FROM_ROWS (chained layers, f1): the plane lists come from the producing gather as
+// per-(plane, row) slots rows[plane*H + r][0..W) with counts rcnt[plane*H + r]
+// (entries (bits, flat index)); each warp first gathers a plane's rows into a
+// contiguous shared list and derives the row prefix from the counts.
+template <bool FROM_ROWS>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
     int H, int W, int TY, int T, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
     uint32_t* __restrict__ offs) {
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
+    extern __shared__ uint2 rowbuf_s[];  // FROM_ROWS: [kPlaneWarps][H*W]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int chunk = blockIdx.x % chunks;
     const int n = blockIdx.x / chunks;
@@ -300,8 +306,21 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     for (int q = 0; q < kPerWarp; ++q) {
         const int ch = warp + q * kPlaneWarps;
         const int plane = n * C + c0 + ch;
-        pv[q] = (ch < nch && lane <= H) ? __ldg(prow + (int64_t)plane * (H + 1) + lane) : 0u;
-        en0[q] = ch < nch ? __ldg(plist + (int64_t)plane * HW + lane) : make_uint2(0u, 0u);
+        if constexpr (FROM_ROWS) {
+            // prow / plist hold the row counts rcnt[plane*H + r] and the row slots
+            const uint32_t rc = (ch < nch && lane < H) ? __ldg(prow + (int64_t)plane * H + lane) : 0u;
+            uint32_t incl = rc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            pv[q] = incl - rc;  // lane r <= H: nonzeros before row r (lane H: the total)
+            en0[q] = make_uint2(0u, 0u);
+        } else {
+            pv[q] = (ch < nch && lane <= H) ? __ldg(prow + (int64_t)plane * (H + 1) + lane) : 0u;
+            en0[q] = ch < nch ? __ldg(plist + (int64_t)plane * HW + lane) : make_uint2(0u, 0u);
+        }
     }
     // ---- stream offsets of this chunk's channels in every tile stream
     for (int t = warp; t < tiles; t += kPlaneWarps) {
@@ -337,6 +356,23 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
         if (ch >= nch) break;
         const int plane = n * C + c0 + ch;
         const uint2* lst = plist + (int64_t)plane * HW;
+        if constexpr (FROM_ROWS) {
+            // gather the plane's row slots into a contiguous shared list (row-major)
+            // list entry k lives in row r(k) = #{r in [1, H] : pv[r] <= k} at slot k - pv[r(k)];
+            // all loads of the plane are independent (lanes over entries)
+            uint2* buf = rowbuf_s + warp * HW;
+            const uint32_t total = __shfl_sync(0xffffffffu, pv[q], H);
+            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                int r = 0;
+                for (int rr = 1; rr <= H; ++rr) r += (__shfl_sync(0xffffffffu, pv[q], rr) <= k) ? 1 : 0;
+                const uint32_t pr = __shfl_sync(0xffffffffu, pv[q], r);
+                if (k < total) buf[k] = __ldg(plist + ((int64_t)plane * H + r) * W + (k - pr));
+            }
+            __syncwarp();
+            lst = buf;
+            en0[q] = lst[lane < HW ? lane : 0];
+        }
         // lane t: run [a, b) of the plane's list inside tile t's window; work = marker + run
         const uint32_t a = __shfl_sync(0xffffffffu, pv[q], r0), b = __shfl_sync(0xffffffffu, pv[q], r1);
         const uint32_t len = lane < tiles ? 1u + (r1 > r0 ? b - a : 0u) : 0u;
@@ -382,11 +418,12 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
                 if (j == 0) {
                     st[p_t] = make_uint2((unsigned)(c0 + ch), (unsigned)NWIN + m_t);
                 } else {
-                    const uint2 e = k < 32 ? ek : __ldg(lst + k);
+                    const uint2 e = k < 32 ? ek : lst[k];
                     st[p_t + j] = make_uint2(e.x, e.y - sh);
                 }
             }
         }
+        if constexpr (FROM_ROWS) __syncwarp();
     }
 }
 
@@ -414,8 +451,45 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
-    compact_plane_emit_kernel<<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
+    compact_plane_emit_kernel<false><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
         plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
+        (int)g.tiles, g.cap, chunks, entries, offs);
+    return cudaGetLastError();
+}
+
+// cnt[n][t][c] = row counts summed over tile t's window rows (chained consumers)
+__global__ void compact_rows_tilecount_kernel(const uint32_t* __restrict__ rcnt, int64_t planes, int C, int H,
+                                              int TYT, int P, int NWR, int tiles, uint32_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= planes * tiles) return;
+    const int64_t plane = i / tiles;
+    const int t = (int)(i - plane * tiles);
+    const int lo = t * TYT - P;
+    const int r0 = lo < 0 ? 0 : lo, r1 = (lo + NWR < H) ? lo + NWR : H;
+    uint32_t acc = 0;
+    for (int r = r0; r < r1; ++r) acc += __ldg(rcnt + plane * H + r);
+    const int64_t n = plane / C;
+    cnt[(n * tiles + t) * C + (plane - n * C)] = acc;
+}
+
+cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt, const uint2* rows,
+                                     const uint32_t* rcnt, uint2* entries, uint32_t* offs, cudaStream_t st) {
+    if (!compact_uses_counts(g)) return cudaErrorNotSupported;
+    const int TYT = (int)(g.ty * g.T);
+    const int64_t planes = n * g.C;
+    compact_rows_tilecount_kernel<<<(unsigned)((planes * g.tiles + 255) / 256), 256, 0, st>>>(
+        rcnt, planes, (int)g.C, (int)g.H, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
+    const size_t smem = sizeof(uint2) * kPlaneWarps * g.H * g.W;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(compact_plane_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    compact_plane_emit_kernel<true><<<(unsigned)(n * chunks), kPlaneWarps * 32, smem, st>>>(
+        rows, rcnt, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
         (int)g.tiles, g.cap, chunks, entries, offs);
     return cudaGetLastError();
 }

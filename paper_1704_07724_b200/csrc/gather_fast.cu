@@ -12,7 +12,8 @@ bool matches(const Geometry& g) {
 }
 #define SC_DECLARE(VV)                                                                                  \
     cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,   \
-                            const float* wpack, const float* bias, float* out, cudaStream_t st);
+                            const float* wpack, const float* bias, float* out, uint2* rowlist,          \
+                            uint32_t* rowcnt, cudaStream_t st);
 SC_GATHER_VARIANTS(SC_DECLARE)
 #undef SC_DECLARE
 }  // namespace fast
@@ -36,11 +37,21 @@ int gather_fast_select(const Geometry& g, int force, const char** name, int* kl,
     return 0;
 }
 
+bool gather_fast_can_emit(int variant) {
+    using namespace fast;
+#define SC_CAN(VV) \
+    if (variant == VV::ID) return !VV::XPAIR;
+    SC_GATHER_VARIANTS(SC_CAN)
+#undef SC_CAN
+    return false;
+}
+
 cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
-                               const float* wpack, const float* bias, float* out, cudaStream_t st) {
+                               const float* wpack, const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt,
+                               cudaStream_t st) {
     using namespace fast;
 #define SC_LAUNCH(VV) \
-    if (variant == VV::ID) return launch_##VV(g, n, entries, offs, wpack, bias, out, st);
+    if (variant == VV::ID) return launch_##VV(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st);
     SC_GATHER_VARIANTS(SC_LAUNCH)
 #undef SC_LAUNCH
     return cudaErrorInvalidValue;

@@ -45,7 +45,9 @@ struct Args {
     const uint32_t* offs;
     const float* wpack;
     const float* bias;
-    float* out;
+    float* out;        // NCHW output; may be null when rowlist is set (chained layers)
+    uint2* rowlist;    // chained layers: the next layer's per-(plane,row) lists
+    uint32_t* rowcnt;  //   [N*K][Ho][WO] entries (bits, y*WO + x) and [N*K][Ho] counts
     int n, C, H, K, Cg, Kg, kblocks, Ho, relu;
     int64_t cap;
     int ytiles, units, ctas_per_kb;
@@ -101,7 +103,7 @@ struct Smem {
     static_assert(total * V::MINB <= 227 * 1024, "shared memory budget of the SM exceeded");
 };
 
-template <class V>
+template <class V, bool EMIT>
 __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(const Args a) {
     using SM = Smem<V>;
     constexpr int RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO;
@@ -255,6 +257,42 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         const int k = kloc + V::KL * lane + h;
         bv[h] = k < a.Kg ? __ldg(&a.bias[g * a.Kg + k]) : 0.0f;
     }
+    if constexpr (EMIT) {
+        // f1: this tile's output rows, after bias and ReLU, compacted per (channel, row) for
+        // the next layer's stage 1 (row-major, as the plane-major compaction would list them)
+        static_assert(!V::XPAIR, "chained list emission needs channel-slot accumulators");
+#pragma unroll
+        for (int h = 0; h < V::KL; ++h) {
+            const int k = kloc + V::KL * lane + h;
+#pragma unroll
+            for (int ty = 0; ty < TY; ++ty) {
+                const int y = y0 + ty;
+                if (k < a.Kg && y < a.Ho) {
+                    const size_t row = ((size_t)n * a.K + (size_t)g * a.Kg + k) * a.Ho + y;
+                    uint2* dst = a.rowlist + row * WO;
+                    uint32_t cnt = 0;
+#pragma unroll
+                    for (int m = 0; m < NX; ++m) {
+                        float o;
+                        if (h < 2 * V::NPAIR) {
+                            const unsigned long long u = accp[ty][m][h / 2];
+                            o = __uint_as_float((h & 1) ? (unsigned)(u >> 32) : (unsigned)u);
+                        } else {
+                            o = accs[ty][m];
+                        }
+                        o += bv[h];
+                        if (a.relu) o = fmaxf(o, 0.f);
+                        if (o != 0.0f) {  // IEEE: -0.0 is zero (R7)
+                            dst[cnt] = make_uint2(__float_as_uint(o), (unsigned)(y * WO + m));
+                            ++cnt;
+                        }
+                    }
+                    a.rowcnt[row] = cnt;
+                }
+            }
+        }
+        if (a.out == nullptr) return;
+    }
 #pragma unroll
     for (int h = 0; h < V::KL; ++h)
 #pragma unroll
@@ -315,11 +353,12 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
 
 template <class V>
 cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs, const float* wpack,
-                     const float* bias, float* out, cudaStream_t st) {
+                     const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt, cudaStream_t st) {
     if (g.ty != V::TY || g.tiles != (g.Ho + V::TY - 1) / V::TY || (g.Cg + V::CH - 1) / V::CH > 63)
         return cudaErrorInvalidValue;
     Args a;
     a.entries = entries; a.offs = offs; a.wpack = wpack; a.bias = bias; a.out = out;
+    a.rowlist = rowlist; a.rowcnt = rowcnt;
     a.n = (int)n; a.C = (int)g.C; a.H = (int)g.H; a.K = (int)g.K; a.Cg = (int)g.Cg; a.Kg = (int)g.Kg;
     a.kblocks = (int)g.kblocks; a.Ho = (int)g.Ho; a.relu = g.relu ? 1 : 0;
     a.cap = g.cap;
@@ -327,7 +366,14 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     a.units = (int)n * a.ytiles;
     a.ctas_per_kb = (a.units + V::NW - 1) / V::NW;
     const size_t smem = Smem<V>::total;
-    auto kern = gather_fast_kernel<V>;
+    auto kern = gather_fast_kernel<V, false>;
+    if (rowlist != nullptr) {
+        if constexpr (V::XPAIR) {
+            return cudaErrorNotSupported;
+        } else {
+            kern = gather_fast_kernel<V, true>;
+        }
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
@@ -343,8 +389,9 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     namespace sc {                                                                                          \
     namespace fast {                                                                                        \
     cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,       \
-                            const float* wpack, const float* bias, float* out, cudaStream_t st) {           \
-        return launch_v<VV>(g, n, entries, offs, wpack, bias, out, st);                                     \
+                            const float* wpack, const float* bias, float* out, uint2* rowlist,              \
+                            uint32_t* rowcnt, cudaStream_t st) {                                            \
+        return launch_v<VV>(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st);                    \
     }                                                                                                       \
     }                                                                                                       \
     }

@@ -44,6 +44,10 @@ cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float
 bool compact_uses_counts(const Geometry& g);
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
                            uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st);
+// Stage 1 of a chained consumer (f1): the producing gather wrote per-(plane, row)
+// lists `rows` [N*C*H][W] and counts `rcnt` [N*C*H]; builds the same R9 streams.
+cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt, const uint2* rows,
+                                     const uint32_t* rcnt, uint2* entries, uint32_t* offs, cudaStream_t st);
 cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
                                   const float* wpack, const float* bias, float* out, cudaStream_t st);
 
@@ -51,9 +55,12 @@ cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* ent
 // variant id > 0 (and its lanes-per-channel KL and tile height TY) if one
 // applies to the geometry, else 0.
 int gather_fast_select(const Geometry& g, int force, const char** name, int* kl, int* ty);
+bool gather_fast_can_emit(int variant);  // the variant can emit chained lists (KL >= 2)
+// rowlist/rowcnt non-null: also emit the next layer's per-(plane,row) lists (f1; KL >= 2 variants);
+// out may then be null.  cudaErrorNotSupported if the variant cannot emit.
 cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries,
                                const uint32_t* offs, const float* wpack, const float* bias, float* out,
-                               cudaStream_t st);
+                               uint2* rowlist, uint32_t* rowcnt, cudaStream_t st);
 
 // Dense tcgen05 TF32 implicit GEMM (dense_tc.cu).
 cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, float* nhwc,

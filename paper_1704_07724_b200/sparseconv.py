@@ -22,7 +22,7 @@ STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_SHAPE", 3: "SC_ER
 EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forward", "dense_conv_forward",
            "sparse_conv_forward_host", "sparse_conv_destroy", "sc_status_string", "sc_last_error",
            "sparse_conv_compact", "sparse_conv_gather", "sparse_conv_lists", "sparse_conv_kernel_variant",
-           "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2")
+           "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain")
 
 
 class SparseConvError(RuntimeError):
@@ -59,6 +59,7 @@ def lib():
         for fn in ("sparse_conv_forward", "dense_conv_forward", "sparse_conv_forward_host"):
             getattr(L, fn).argtypes = [vp, i64, vp, vp, vp]
         L.sparse_conv_compact.argtypes = [vp, i64, vp, vp]
+        L.sparse_conv_forward_chain.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64, vp, ctypes.POINTER(vp), vp]
         L.sparse_conv_gather.argtypes = [vp, i64, vp, vp]
         L.sparse_conv_destroy.argtypes = [vp]
         L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
@@ -214,6 +215,25 @@ class SparseConv:
             self.close()
         except Exception:
             pass
+
+
+def chain_forward(convs, x, outs, stream=None):
+    """Run a chain of SparseConv layers (sparse_conv_forward_chain).  outs[l]:
+    output tensor of layer l, or None for an intermediate layer whose epilogue
+    should emit the next layer's stage-1 lists instead of a dense output.
+    outs[-1] must be a tensor.  Returns outs[-1]."""
+    n = x.shape[0]
+    _check_tensor(x, "x", convs[0].device, (n,) + convs[0].in_shape)
+    for l, (c, o) in enumerate(zip(convs, outs)):
+        if o is not None:
+            _check_tensor(o, f"outs[{l}]", c.device, (n,) + c.out_shape)
+    if outs[-1] is None:
+        raise ValueError("the last layer needs an output tensor")
+    plans = (ctypes.c_void_p * len(convs))(*[c._plan.value for c in convs])
+    ptrs = (ctypes.c_void_p * len(outs))(*[None if o is None else o.data_ptr() for o in outs])
+    _check(lib().sparse_conv_forward_chain(plans, len(convs), n, ctypes.c_void_p(x.data_ptr()), ptrs,
+                                           _stream_handle(stream)))
+    return outs[-1]
 
 
 def probe_fma(kind):

@@ -54,3 +54,54 @@ def test_c5_chain_small_batch_all_images():
 
 def test_c5_chain_full_batch_sampled_images():
     run_chain(1024, [0, 511, 1023])
+
+
+def _chain_setup(n):
+    from paper_1704_07724_b200 import sparseconv as sc
+    layers = [shp.with_batch(n) for shp in datagen.C5_LAYERS]
+    weights = datagen.c5_weights()
+    convs = []
+    for li, shp in enumerate(layers):
+        w, b = weights[li]
+        convs.append(sc.SparseConv(torch.from_numpy(w).to(DEV), torch.from_numpy(b).to(DEV), n, shp.c, shp.h, shp.w,
+                                   shp.stride, shp.pad, shp.groups, fuse_relu=li + 1 < len(layers)))
+    x = torch.from_numpy(datagen.activations(layers[0], datagen.C5_FIRST_SPARSITY)).to(DEV)
+    return sc, layers, weights, convs, x
+
+
+@pytest.mark.parametrize("n", [3, 64])
+def test_chain_fused_lists_match_compaction_and_oracle(n):
+    """f1: intermediate layers emit the next layer's stage-1 lists from
+    their epilogue.  With the intermediate outputs also materialised, every
+    consumer's R9 streams must equal oracle.compact_streams of the producer's
+    output bit for bit, and every layer must meet the tolerance on its own
+    input (R14); without them the final output must be bit-identical."""
+    sc, layers, weights, convs, x = _chain_setup(n)
+    outs = [torch.empty((n,) + c.out_shape, device=DEV) for c in convs]
+    sc.chain_forward(convs, x, outs)
+    torch.cuda.synchronize()
+    inputs = [x] + outs[:-1]
+    for li, (shp, conv) in enumerate(zip(layers, convs)):
+        xin = inputs[li].cpu().numpy()
+        lists = conv.lists(n)
+        ref_l = oracle.compact_streams(xin, shp.r, shp.stride, shp.pad, lists["ty"])
+        offs = lists["offs"].cpu().numpy().view(np.uint32)
+        assert np.array_equal(offs, ref_l["offs"]), f"layer {li}: stream offsets"
+        length = ref_l["offs"][:, :, -1]
+        valid = np.arange(ref_l["cap"])[None, None, :] < length[:, :, None]
+        ge = lists["entries"].cpu().numpy().view(np.uint32)
+        assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref_l["entries"], 0)), \
+            f"layer {li}: stream entries"
+        w, b = weights[li]
+        got = outs[li].cpu().numpy()
+        for i in sorted({0, n - 1}):
+            ref, mass = oracle.conv_fp64(xin[i:i + 1], w, b, shp.stride, shp.pad, shp.groups)
+            if li + 1 < len(layers):
+                ref = np.maximum(ref, 0.0)
+            err = np.abs(got[i:i + 1].astype(np.float64) - ref) / oracle.tolerance_sparse(mass)
+            assert err.max() <= 1.0, f"layer {li} image {i}: max err/tol {err.max():.3f}"
+    # fused only: no intermediate dense tensors, same final bits
+    fin = torch.empty_like(outs[-1])
+    sc.chain_forward(convs, x, [None] * (len(convs) - 1) + [fin])
+    torch.cuda.synchronize()
+    assert torch.equal(fin, outs[-1])

@@ -1,1 +1,1 @@
-timeout 600 python tools/variant_sweep.py C2 0.95,0.99 "21 34 35" > gpurun_out/sweep.log 2>&1; echo sweep=$?
+timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5.log 2>&1; echo bench_c5=$?
