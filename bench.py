@@ -535,6 +535,50 @@ def run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
     return 0
 
 
+# Paper Table 3: Xeon E5-2630v4 CPU, Caffe+MKL GEMM vs ISC, ms and printed speedup.
+# Context only (another machine, batch size unstated).
+PAPER_TABLE3 = {"LeNet-Conv2": (0.854, 0.123, 6.96), "AlexNetC-Conv3": (0.329, 0.122, 2.69),
+                "AlexNetI-Conv4": (4.874, 1.660, 2.94), "GoogLeNet-Inception4a.1": (1.795, 1.292, 1.39),
+                "GoogLeNet-Inception4a.2": (0.943, 0.558, 1.69), "GoogLeNet-Inception4e.3": (7.602, 4.782, 1.59),
+                "GoogLeNet-Inception5a.1": (1.912, 0.645, 2.97), "GoogLeNet-Inception5a.2": (0.742, 0.258, 2.87),
+                "GoogLeNet-Inception5b.3": (4.410, 0.931, 4.74), "GoogLeNet-Inception5b.5": (1.560, 0.220, 7.11)}
+
+
+def run_table2(args):
+    """B200 analogue of the paper's Table 3: every Table 2 layer
+     at its printed sparsity, N=128 synthetic images: the sparse
+    forward (both stages) vs the in-library tcgen05 dense convolution, device
+    times from CUDA graphs of back-to-back launches."""
+    import torch
+    from paper_1704_07724_b200 import sparseconv as sc
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    rows = []
+    for shp, s in datagen.table2_shapes(n=args.table2_batch):
+        x = torch.from_numpy(datagen.activations(shp, s)).to(dev)
+        w, b = datagen.weights(shp)
+        conv = sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), shp.n, shp.c, shp.h, shp.w,
+                             shp.stride, shp.pad, shp.groups)
+        out = torch.empty((shp.n,) + conv.out_shape, device=dev)
+        t_s = graph_time_us(torch, stream, lambda: conv.forward(x, out, stream=stream))
+        try:
+            t_d = graph_time_us(torch, stream, lambda: conv.dense_forward(x, out, stream=stream), reps=5)
+        except sc.SparseConvError:
+            t_d = None
+        dense, exact, nnz = mac_counts(x, shp)
+        cpu = PAPER_TABLE3.get(shp.name)
+        rows.append({"layer": shp.name, "shape": f"{shp.c}x{shp.h}x{shp.w}->{shp.k} {shp.r}x{shp.s} p{shp.pad} "
+                                                 f"t{shp.stride}", "s": s, "variant": conv.variant[1],
+                     "sparse_us": round(t_s, 2), "dense_tc_us": None if t_d is None else round(t_d, 2),
+                     "b200_speedup_sparse_over_dense": None if t_d is None else round(t_d / t_s, 3),
+                     "sparse_frac_fp32": round(2 * exact / (t_s * 1e-6) / 1e12 / FP32_PEAK_TFLOPS, 4),
+                     "paper_cpu_gemm_ms": cpu[0] if cpu else None, "paper_cpu_isc_ms": cpu[1] if cpu else None,
+                     "paper_cpu_speedup": cpu[2] if cpu else None})
+    print(json.dumps({"table2": rows, "batch": args.table2_batch, "data": "synthetic",
+                      "note": "paper_cpu_* from PAPER.md Table 3 (Xeon E5-2630v4), context only"}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -545,7 +589,11 @@ def main():
     ap.add_argument("--sparsity", type=float, default=0.95)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--table2", action="store_true", help="paper Table 2 layers: sparse vs dense on B200")
+    ap.add_argument("--table2-batch", type=int, default=128)
     args = ap.parse_args()
+    if args.table2:
+        return run_table2(args)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -7,7 +7,7 @@ namespace fast {
 #include "gather_variants.inc"
 template <class V>
 bool matches(const Geometry& g) {
-    return g.T == 1 && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1 &&
+    return g.T == V::T && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1 &&
            (g.Cg + V::CH - 1) / V::CH <= 63;
 }
 #define SC_DECLARE(VV)                                                                                  \

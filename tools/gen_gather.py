@@ -55,6 +55,15 @@ VARIANTS = [
     (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a
     (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
     (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
+    # paper Table 2 shapes: stride 2, 1x1, small planes
+    (40, "r5s5p1t2_w11_ty5_kl2", 5, 5, 1, 11, 5, 2, 11, 1, 8, 2, None, 3, 254, 2),  # LeNet-Conv2 (T=2)
+    (41, "r5s5p2_w6_ty6_kl2", 5, 5, 2, 6, 6, 2, 11, 1, 8, 2),                       # AlexNetC-Conv3
+    (42, "r3s3p1_w5_ty5_kl4", 3, 3, 1, 5, 5, 4, 11, 1, 16, 2),                      # AlexNetI-Conv4
+    (43, "r1s1p0_w14_ty2_kl4", 1, 1, 0, 14, 2, 4, 11, 1, 32, 2),                    # Inception4a.1/.2
+    (44, "r3s3p1_w14_ty2_kl4", 3, 3, 1, 14, 2, 4, 11, 1, 16, 2),                    # Inception4e.3
+    (45, "r1s1p0_w7_ty3_kl4", 1, 1, 0, 7, 3, 4, 11, 1, 32, 2),                      # Inception5a.1/.2
+    (46, "r3s3p1_w7_ty3_kl4", 3, 3, 1, 7, 3, 4, 11, 1, 16, 2),                      # Inception5b.3
+    (47, "r5s5p2_w7_ty5_kl2", 5, 5, 2, 7, 5, 2, 11, 1, 8, 2),                       # Inception5b.5
     (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),        # C4b
 ]
 
@@ -68,13 +77,14 @@ ABLATIONS = [
 PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4, 33, 3]
 
 
-def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254):
-    WO = W + 2 * P - S + 1
+def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1):
+    WO = (W + 2 * P - S) // T + 1
     XPAIR = KL == 1
+    assert not (XPAIR and T != 1), "x-pair tiles assume stride 1"
     NX = (WO + 1) // 2 if XPAIR else WO            # accumulator columns per row
     NPAIR = 1 if XPAIR else KL // 2                 # f32x2 accumulators per (ty, m)
     NSING = 0 if XPAIR else KL % 2                  # f32 accumulators per (ty, m)
-    NWR = TY + R - 1                                 # window rows
+    NWR = (TY - 1) * T + R                           # window rows (R9)
     NCASES = NWR * W
     ops = []                                         # asm operand list: (constraint, C++ expression)
     accp = {}
@@ -119,12 +129,12 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
         for j in range(W):
             body = []
             for ty in range(TY):
-                r = wi - ty
+                r = wi - ty * T   # window row wi = ty*T + r (R9)
                 if not (0 <= r < R):
                     continue
                 if not XPAIR:
                     for x in range(WO):
-                        t = j + P - x
+                        t = j + P - x * T
                         if 0 <= t < S:
                             for pi in range(NPAIR):
                                 a = accp[(ty, x, pi)]
@@ -258,7 +268,7 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
     lines = [f"// ---- variant {vid}: {name}  (R={R} S={S} P={P} W={W} WO={WO} TY={TY} KL={KL} NX={NX} NW={NW}); "
              f"{n_fma} FMA instructions over {NCASES} window positions"]
     lines.append(f"struct V{vid} {{")
-    for k, v in (("R", R), ("S", S), ("P", P), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
+    for k, v in (("R", R), ("S", S), ("P", P), ("T", T), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
                  ("NW", NW), ("MINB", MINB), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
                  ("NPAIR", NPAIR), ("NSING", NSING), ("NWP", len(wp)), ("NWS", max(1, len(ws))),
                  ("SLOTS", SLOTS), ("PIECE", PIECE)):

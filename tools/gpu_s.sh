@@ -1,1 +1,2 @@
-timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5.log 2>&1; echo bench_c5=$?
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --table2 > gpurun_out/table2.log 2>&1; echo table2=$?
