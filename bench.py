@@ -309,6 +309,8 @@ def run_single(args, torch, dev, ws, rank, sc):
     lists_per_batch = n * conv.lists(1)["tiles"] * shp.c
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     stream = torch.cuda.Stream(dev)
+    # f3: measured crossover sparsity for this batch (before any capture)
+    conv.s_star_calibrated = conv.calibrate_crossover(n, stream)
 
     def measure(s, steps, warmup):
         per_set = 4 * n * (shp.c * shp.h * shp.w + shp.k * shp.ho * shp.wo)
@@ -335,6 +337,9 @@ def run_single(args, torch, dev, ws, rank, sc):
         res["gather_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
         res["dense_tc_us"] = graph_time_us(torch, stream, lambda: conv.dense_forward(xs[0], outs[0], stream=stream),
                                            reps=5)
+        res["auto_us"] = graph_time_us(torch, stream, lambda: conv.forward_auto(xs[0], outs[0], stream=stream),
+                                       reps=5)
+        res["auto_path"] = "sparse" if conv.last_path()[0] == sc.SC_PATH_SPARSE else "dense"
         dense = sum(c[0] for c in counts) / nsets
         exact = sum(c[1] for c in counts) / nsets
         nnz = sum(c[2] for c in counts) / nsets
@@ -425,8 +430,13 @@ def run_ours(args):
                            "gather_frac_fp32": round(2 * r["exact_set0"] / (r["gather_us"] * 1e-6) / 1e12
                                                      / FP32_PEAK_TFLOPS, 4),
                            "gather_us": round(r["gather_us"], 3), "compact_us": round(r["compact_us"], 3),
-                           "dense_tc_speedup": round(r["dense_tc_us"] / (r["ms_per_step"] * 1e3), 3)}
+                           "dense_tc_speedup": round(r["dense_tc_us"] / (r["ms_per_step"] * 1e3), 3),
+                           "auto_us": round(r["auto_us"], 3), "auto_path": r["auto_path"]}
                   for s, r in sweep.items()},
+        "crossover": {"s_star": round(conv.s_star_calibrated, 4), "auto_us": round(v["auto_us"], 3),
+                      "auto_path": v["auto_path"],
+                      "note": "sparse_conv_forward_auto: device-side nnz count picks sparse iff s >= s*; s* "
+                              "calibrated by sparse_conv_calibrate_crossover for this batch (SURVEY 8f row f3)"},
         "e2e": {"value": round(gflops(v["dense"], e2e_s * 1e3), 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int(h_in.numel() * 4), "d2h_bytes_per_step": int(h_out.numel() * 4),
                 "ms_per_step": round(e2e_s * 1e3, 4), "api": "sparse_conv_forward_host (pinned host buffers)"},
@@ -565,12 +575,16 @@ def run_table2(args):
             t_d = graph_time_us(torch, stream, lambda: conv.dense_forward(x, out, stream=stream), reps=5)
         except sc.SparseConvError:
             t_d = None
+        s_star = conv.calibrate_crossover(shp.n, stream)
+        t_a = graph_time_us(torch, stream, lambda: conv.forward_auto(x, out, stream=stream), reps=5)
+        path = "sparse" if conv.last_path()[0] == sc.SC_PATH_SPARSE else "dense"
         dense, exact, nnz = mac_counts(x, shp)
         cpu = PAPER_TABLE3.get(shp.name)
         rows.append({"layer": shp.name, "shape": f"{shp.c}x{shp.h}x{shp.w}->{shp.k} {shp.r}x{shp.s} p{shp.pad} "
                                                  f"t{shp.stride}", "s": s, "variant": conv.variant[1],
                      "sparse_us": round(t_s, 2), "dense_tc_us": None if t_d is None else round(t_d, 2),
                      "b200_speedup_sparse_over_dense": None if t_d is None else round(t_d / t_s, 3),
+                     "s_star": round(s_star, 4), "auto_us": round(t_a, 2), "auto_path": path,
                      "sparse_frac_fp32": round(2 * exact / (t_s * 1e-6) / 1e12 / FP32_PEAK_TFLOPS, 4),
                      "paper_cpu_gemm_ms": cpu[0] if cpu else None, "paper_cpu_isc_ms": cpu[1] if cpu else None,
                      "paper_cpu_speedup": cpu[2] if cpu else None})

@@ -152,6 +152,45 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, f
 sc_status sparse_conv_forward_chain(const sc_plan *plans, int32_t nplans, int64_t n, const float *d_in,
                                     float *const *d_outs, sc_stream_t stream);
 
+/* ---- automatic sparse <-> dense crossover --------------
+ * The paper claims its speedup "when the sparsity is not less than 0.9"
+ * (P:23): the sparse method pays off only above a crossover sparsity
+ * s*, which on B200 depends on the shape and the batch (the dense path runs on
+ * tensor cores).  sparse_conv_forward_auto decides per call ON THE DEVICE:
+ * one kernel counts the batch's nonzero inputs (sparsity s = 1 - nnz/(n*C*H*W))
+ * and writes a path flag; the sparse path (s >= s*) and the dense path
+ * (s < s*) are both enqueued and the kernels of the path not chosen return at
+ * once.  No host synchronization: capturable like sparse_conv_forward (after
+ * calibration).  Plans whose dense path is unsupported always run sparse. */
+#define SC_PATH_SPARSE 0
+#define SC_PATH_DENSE 1
+
+/* Same buffer and stream contract as sparse_conv_forward.  If the plan has no
+ * crossover yet (neither set nor calibrated), calibrates it first with
+ * sparse_conv_calibrate_crossover(plan, n, stream) (synchronizes; returns
+ * SC_ERR_INVALID_ARGUMENT if `stream` is capturing). */
+sc_status sparse_conv_forward_auto(sc_plan plan, int64_t n, const float *d_in, float *d_out,
+                                   sc_stream_t stream);
+
+/* Measure s* for batches of n images on this device: times the dense path
+ * and the sparse path on plan-owned synthetic inputs (i.i.d. nonzeros,
+ * counter-based hash) at several sparsities, locates the sparsity where the
+ * two times are equal (bracketing secant on the measured sparse time), stores
+ * it in the plan and returns it in *s_star (may be NULL).  s* = 1 means "always
+ * dense", 0 "always sparse".  Allocates the plan's staging buffers (as
+ * sparse_conv_forward_host) on first use; synchronizes `stream`. */
+sc_status sparse_conv_calibrate_crossover(sc_plan plan, int64_t n, sc_stream_t stream, double *s_star);
+
+/* Set s* in [0, 1] explicitly (no calibration), or query it (*s_star < 0: not
+ * set yet). */
+sc_status sparse_conv_set_crossover(sc_plan plan, double s_star);
+sc_status sparse_conv_get_crossover(sc_plan plan, double *s_star);
+
+/* Which path the last sparse_conv_forward_auto on this plan took
+ * (SC_PATH_SPARSE / SC_PATH_DENSE) and the nonzero count it measured.
+ * Synchronizes the device. */
+sc_status sparse_conv_last_path(sc_plan plan, int32_t *path, int64_t *nnz);
+
 /* Free everything the plan owns.  NULL is a no-op. */
 sc_status sparse_conv_destroy(sc_plan plan);
 
@@ -176,7 +215,9 @@ sc_status sparse_conv_lists(sc_plan plan, sc_lists_view *out);
  * stride/shape), >0 = a shape-specialised register-tile kernel variant id. */
 sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t *variant, const char **name);
 
-/* Number of kernels one sparse_conv_forward / dense_conv_forward launches. */
+/* Number of kernels one sparse_conv_forward / dense_conv_forward launches
+ * (sparse_conv_forward_auto launches 1 + both when the dense path is
+ * supported, else 1 + sparse). */
 sc_status sparse_conv_launch_count(sc_plan plan, int32_t *sparse_launches, int32_t *dense_launches);
 
 /* Micro-probes for the roofline denominators (bench only).  Each runs on the

@@ -31,9 +31,12 @@ struct sc_plan_s {
     uint32_t* prow = nullptr;  // stage-1 per-plane row prefixes [N*C][H+1]
     int variant = 0;
     const char* variant_name = "generic";
-    // staging for sparse_conv_forward_host (allocated on first use)
+    // staging for sparse_conv_forward_host and calibration (allocated on first use)
     float* stage_in = nullptr;
     float* stage_out = nullptr;
+    // f3 crossover: device words (nnz, ticket, path flag, last nnz) and s* (< 0: unset)
+    unsigned long long* sel = nullptr;
+    double s_star = -1.0;
 };
 
 namespace {
@@ -160,7 +163,76 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->prow);
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
+    cudaFree(p->sel);
     delete p;
+}
+
+// stage 1 + stage 2 of the sparse path (gated: f3)
+cudaError_t enqueue_sparse(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
+                           sc::Gate gate = {}) {
+    cudaError_t e = sc::launch_compact(p->g, n, d_in, p->cnt, p->plist, p->prow, p->entries, p->offs, s, gate);
+    if (e != cudaSuccess) return e;
+    if (p->variant > 0)
+        return sc::launch_gather_fast(p->variant, p->g, n, p->entries, p->offs, p->wpack, p->bias, d_out, nullptr,
+                                      nullptr, s, gate);
+    return sc::launch_gather_generic(p->g, n, p->entries, p->offs, p->wpack, p->bias, d_out, s, gate);
+}
+
+cudaError_t enqueue_dense(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
+                          sc::Gate gate = {}) {
+    return sc::launch_dense_tc(p->g, p->dg, n, d_in, p->nhwc, p->bmap, p->wdense, p->bias, d_out, s, gate);
+}
+
+cudaError_t ensure_staging(sc_plan_s* p) {
+    const Geometry& g = p->g;
+    cudaError_t e;
+    if (!p->stage_in && (e = cudaMalloc(&p->stage_in, sizeof(float) * g.N * g.C * g.H * g.W)) != cudaSuccess) return e;
+    if (!p->stage_out && (e = cudaMalloc(&p->stage_out, sizeof(float) * g.N * g.K * g.Ho * g.Wo)) != cudaSuccess)
+        return e;
+    return cudaSuccess;
+}
+
+// Best-of-3 device time (us) of one path on the staged input (one untimed run first).
+cudaError_t time_path(sc_plan_s* p, int64_t n, bool dense, cudaStream_t s, double* us) {
+    cudaEvent_t a, b;
+    cudaError_t e = cudaEventCreate(&a);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventCreate(&b)) != cudaSuccess) {
+        cudaEventDestroy(a);
+        return e;
+    }
+    double best = 1e30;
+    for (int it = 0; it < 4 && e == cudaSuccess; ++it) {
+        if ((e = cudaEventRecord(a, s)) != cudaSuccess) break;
+        e = dense ? enqueue_dense(p, n, p->stage_in, p->stage_out, s) : enqueue_sparse(p, n, p->stage_in, p->stage_out, s);
+        if (e != cudaSuccess) break;
+        if ((e = cudaEventRecord(b, s)) != cudaSuccess || (e = cudaEventSynchronize(b)) != cudaSuccess) break;
+        float ms = 0;
+        if ((e = cudaEventElapsedTime(&ms, a, b)) != cudaSuccess) break;
+        if (it > 0 && ms * 1e3 < best) best = ms * 1e3;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us = best;
+    return e;
+}
+
+// Sparse-path time minus dense-path time at input density rho (f3 calibration).
+cudaError_t sparse_minus_dense(sc_plan_s* p, int64_t n, double rho, double dense_us, cudaStream_t s, double* f) {
+    const int64_t elems = n * p->g.C * p->g.H * p->g.W;
+    cudaError_t e = sc::launch_synth_relu(p->stage_in, elems, rho, 0x5eed1234u, s);
+    if (e != cudaSuccess) return e;
+    double us = 0;
+    if ((e = time_path(p, n, false, s, &us)) != cudaSuccess) return e;
+    *f = us - dense_us;
+    return cudaSuccess;
+}
+
+// Largest nonzero count the sparse path is taken for: s >= s* <=> nnz <= (1 - s*) * elems.
+unsigned long long auto_threshold(const sc_plan_s* p, int64_t elems) {
+    if (!p->dg.supported) return ~0ull;
+    const double lim = (1.0 - p->s_star) * (double)elems;
+    return lim <= 0 ? 0ull : (unsigned long long)lim;
 }
 
 sc_status check_forward(sc_plan plan, int64_t n) {
@@ -236,6 +308,7 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         (e = cudaMalloc(&plan->bias, sizeof(float) * g.K)) != cudaSuccess ||
         (e = cudaMalloc(&plan->entries, sizeof(uint2) * (g.N * g.tiles * g.cap + 2))) != cudaSuccess ||
         (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&plan->sel, 4 * sizeof(unsigned long long))) != cudaSuccess ||
         (sc::compact_uses_counts(g) &&
          ((e = cudaMalloc(&plan->cnt, sizeof(uint32_t) * g.N * g.tiles * g.C)) != cudaSuccess ||
           (e = cudaMalloc(&plan->plist, sizeof(uint2) * g.N * g.C * g.H * g.W)) != cudaSuccess ||
@@ -251,6 +324,7 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     // stream slack is never interpreted, but the stage-2 bulk copies round
     // piece boundaries to 16 bytes: keep the workspace initialised
     if (e == cudaSuccess) e = cudaMemsetAsync(plan->entries, 0, sizeof(uint2) * (g.N * g.tiles * g.cap + 2), st0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(plan->sel, 0, 4 * sizeof(unsigned long long), st0);
     if (e == cudaSuccess) e = sc::launch_pack_weights(g, d_weight, plan->wpack, st0);
     if (e == cudaSuccess) e = sc::launch_pack_dense(g, dg, d_weight, plan->wdense, st0);
     if (e == cudaSuccess && dg.supported) e = sc::encode_dense_input_map(g, dg, plan->nhwc, plan->bmap);
@@ -275,7 +349,8 @@ sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float* d_in, sc_str
     if (st != SC_OK) return st;
     if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
-    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, plan->entries, plan->offs, (cudaStream_t)stream);
+    cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, plan->entries,
+                                       plan->offs, (cudaStream_t)stream);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "compact launch");
 }
 
@@ -306,8 +381,7 @@ sc_status dense_conv_forward(sc_plan plan, int64_t n, const float* d_in, float* 
     if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
     if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
-    cudaError_t e = sc::launch_dense_tc(plan->g, plan->dg, n, d_in, plan->nhwc, plan->bmap, plan->wdense, plan->bias,
-                                        d_out, (cudaStream_t)stream);
+    cudaError_t e = enqueue_dense(plan, n, d_in, d_out, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) return fail(SC_ERR_UNSUPPORTED, "dense path: shape not supported");
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "dense launch");
 }
@@ -318,12 +392,8 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
     if (!h_in || !h_out) return fail(SC_ERR_INVALID_ARGUMENT, "host buffer is NULL");
     DeviceGuard guard(plan->device);
     const Geometry& g = plan->g;
-    const size_t in_b = sizeof(float) * g.N * g.C * g.H * g.W, out_b = sizeof(float) * g.N * g.K * g.Ho * g.Wo;
     cudaError_t e;
-    if (!plan->stage_in) {
-        if ((e = cudaMalloc(&plan->stage_in, in_b)) != cudaSuccess) return cuda_fail(e, "staging alloc");
-        if ((e = cudaMalloc(&plan->stage_out, out_b)) != cudaSuccess) return cuda_fail(e, "staging alloc");
-    }
+    if ((e = ensure_staging(plan)) != cudaSuccess) return cuda_fail(e, "staging alloc");
     cudaStream_t s = (cudaStream_t)stream;
     const size_t nin = sizeof(float) * n * g.C * g.H * g.W, nout = sizeof(float) * n * g.K * g.Ho * g.Wo;
     if ((e = cudaMemcpyAsync(plan->stage_in, h_in, nin, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -385,6 +455,113 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
         if (e != cudaSuccess) return cuda_fail(e, "chain gather");
         lists_ready = emit;
     }
+    return SC_OK;
+}
+
+sc_status sparse_conv_calibrate_crossover(sc_plan plan, int64_t n, sc_stream_t stream, double* s_star) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cap);
+    if (e != cudaSuccess) return cuda_fail(e, "calibrate: capture query");
+    if (cap != cudaStreamCaptureStatusNone)
+        return fail(SC_ERR_INVALID_ARGUMENT, "calibrate: stream is capturing (calibrate before capture)");
+    if (!plan->dg.supported) {
+        plan->s_star = 0.0;  // no dense path: always sparse
+            if (s_star) *s_star = plan->s_star;
+        return SC_OK;
+    }
+    if ((e = ensure_staging(plan)) != cudaSuccess) return cuda_fail(e, "staging alloc");
+    const int64_t elems = n * plan->g.C * plan->g.H * plan->g.W;
+    double dense_us = 0;
+    if ((e = sc::launch_synth_relu(plan->stage_in, elems, 0.5, 1u, s)) != cudaSuccess ||
+        (e = time_path(plan, n, true, s, &dense_us)) != cudaSuccess)
+        return cuda_fail(e, "calibrate: dense timing");
+    // f(rho) = t_sparse(rho) - t_dense, increasing in the density rho = 1 - s
+    double lo = 0.0, flo = 0, hi = 0.1, fhi = 0;
+    if ((e = sparse_minus_dense(plan, n, lo, dense_us, s, &flo)) != cudaSuccess) return cuda_fail(e, "calibrate");
+    double rho_star;
+    if (flo >= 0) {
+        rho_star = 0.0;  // sparse loses even on an all-zero input: always dense
+    } else {
+        if ((e = sparse_minus_dense(plan, n, hi, dense_us, s, &fhi)) != cudaSuccess) return cuda_fail(e, "calibrate");
+        while (fhi < 0 && hi < 1.0) {
+            lo = hi;
+            flo = fhi;
+            hi = hi * 2 < 1.0 ? hi * 2 : 1.0;
+            if ((e = sparse_minus_dense(plan, n, hi, dense_us, s, &fhi)) != cudaSuccess) return cuda_fail(e, "calibrate");
+        }
+        if (fhi < 0) {
+            rho_star = 1.0;  // sparse wins even on a dense input: always sparse
+        } else {
+            // regula falsi (Illinois) on the bracket [lo, hi]
+            int side = 0;
+            for (int it = 0; it < 5; ++it) {
+                const double m = lo + (hi - lo) * (-flo) / (fhi - flo);
+                double fm = 0;
+                if ((e = sparse_minus_dense(plan, n, m, dense_us, s, &fm)) != cudaSuccess)
+                    return cuda_fail(e, "calibrate");
+                if (fm < 0) {
+                    lo = m;
+                    flo = fm;
+                    if (side == -1) fhi *= 0.5;
+                    side = -1;
+                } else {
+                    hi = m;
+                    fhi = fm;
+                    if (side == 1) flo *= 0.5;
+                    side = 1;
+                }
+                if (hi - lo < 1e-3) break;
+            }
+            rho_star = lo + (hi - lo) * (-flo) / (fhi - flo);
+        }
+    }
+    plan->s_star = 1.0 - rho_star;
+    if (s_star) *s_star = plan->s_star;
+    return SC_OK;
+}
+
+sc_status sparse_conv_set_crossover(sc_plan plan, double s_star) {
+    if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (!(s_star >= 0.0 && s_star <= 1.0)) return fail(SC_ERR_INVALID_ARGUMENT, "s_star outside [0, 1]");
+    plan->s_star = s_star;
+    return SC_OK;
+}
+
+sc_status sparse_conv_get_crossover(sc_plan plan, double* s_star) {
+    if (!plan || !s_star) return fail(SC_ERR_INVALID_ARGUMENT, "NULL argument");
+    *s_star = plan->s_star;
+    return SC_OK;
+}
+
+sc_status sparse_conv_forward_auto(sc_plan plan, int64_t n, const float* d_in, float* d_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK) return st;
+    if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
+    if (plan->s_star < 0 && (st = sparse_conv_calibrate_crossover(plan, n, stream, nullptr)) != SC_OK) return st;
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t elems = n * plan->g.C * plan->g.H * plan->g.W;
+    const int* flag = reinterpret_cast<const int*>(plan->sel + 2);
+    cudaError_t e = sc::launch_select_path(d_in, elems, auto_threshold(plan, elems), plan->sel, s);
+    if (e == cudaSuccess) e = enqueue_sparse(plan, n, d_in, d_out, s, sc::Gate{flag, sc::kPathSparse});
+    if (e == cudaSuccess && plan->dg.supported)
+        e = enqueue_dense(plan, n, d_in, d_out, s, sc::Gate{flag, sc::kPathDense});
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "auto forward launch");
+}
+
+sc_status sparse_conv_last_path(sc_plan plan, int32_t* path, int64_t* nnz) {
+    if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    DeviceGuard guard(plan->device);
+    unsigned long long h[4];
+    cudaError_t e = cudaMemcpy(h, plan->sel, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "last_path copy");
+    if (path) *path = (int32_t)(h[2] & 0xffffffffu);
+    if (nnz) *nnz = (int64_t)h[3];
     return SC_OK;
 }
 

@@ -44,7 +44,8 @@ template <int KV>
 __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __restrict__ in, int C, int H, int W,
                                                                int TY, int tiles, int T, int P, int NWR, int NWIN,
                                                                int64_t cap, uint2* __restrict__ entries,
-                                                               uint32_t* __restrict__ offs) {
+                                                               uint32_t* __restrict__ offs, Gate gate) {
+    if (gate_closed(gate)) return;
     constexpr int RCH = kRegs / KV;  // channels per warp per round
     constexpr int BLK = 32 * KV;     // floats per load block
     __shared__ uint32_t start_s[32 * RCH];
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
 }
 
 static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const float* in, uint2* entries,
-                                            uint32_t* offs, cudaStream_t st) {
+                                            uint32_t* offs, cudaStream_t st, Gate gate) {
     const int64_t rows = g.nwr < g.H ? g.nwr : g.H;
     const int64_t seg = rows * g.W;
     const int kv = seg <= 32 ? 1 : seg <= 64 ? 2 : seg <= 128 ? 4 : 8;
@@ -199,7 +200,7 @@ static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const
 #define SC_LAUNCH_KV(K)                                                                                            \
     compact_streams_kernel<K><<<grid, threads, 0, st>>>(in, (int)g.C, (int)g.H, (int)g.W, (int)g.ty,               \
                                                         (int)g.tiles, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, \
-                                                        g.cap, entries, offs)
+                                                        g.cap, entries, offs, gate)
     if (kv == 1) SC_LAUNCH_KV(1);
     else if (kv == 2) SC_LAUNCH_KV(2);
     else if (kv == 4) SC_LAUNCH_KV(4);
@@ -235,7 +236,8 @@ constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 template <int NSLOT>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const float* __restrict__ in, int planes, int C, int H, int W, int TYT, int P, int NWR, int tiles,
-    uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow) {
+    uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow, Gate gate) {
+    if (gate_closed(gate)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int plane = blockIdx.x * kPlaneWarps + warp;
     if (plane >= planes) return;
@@ -288,7 +290,8 @@ template <bool FROM_ROWS>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
     int H, int W, int TY, int T, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
-    uint32_t* __restrict__ offs) {
+    uint32_t* __restrict__ offs, Gate gate) {
+    if (gate_closed(gate)) return;
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
     extern __shared__ uint2 rowbuf_s[];  // FROM_ROWS: [kPlaneWarps][H*W]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -428,9 +431,9 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
 }
 
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
-                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st) {
+                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate) {
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
-        return launch_compact_streamwise(g, n, in, entries, offs, st);
+        return launch_compact_streamwise(g, n, in, entries, offs, st, gate);
     const int TYT = (int)(g.ty * g.T);
     const int planes = (int)(n * g.C);
     const unsigned cgrid = (unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps);
@@ -439,7 +442,7 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
 #define SC_COUNT(NS)                                                                                             \
     compact_plane_count_kernel<NS><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, planes, (int)g.C, (int)g.H, (int)g.W, \
                                                                        TYT, (int)g.P, (int)g.nwr, (int)g.tiles,   \
-                                                                       cnt, plist, prow)
+                                                                       cnt, plist, prow, gate)
     if (slots <= 2) SC_COUNT(2);
     else if (slots <= 4) SC_COUNT(4);
     else if (slots <= 6) SC_COUNT(6);
@@ -453,7 +456,7 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
     compact_plane_emit_kernel<false><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
         plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-        (int)g.tiles, g.cap, chunks, entries, offs);
+        (int)g.tiles, g.cap, chunks, entries, offs, gate);
     return cudaGetLastError();
 }
 
@@ -490,7 +493,7 @@ cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt
     }
     compact_plane_emit_kernel<true><<<(unsigned)(n * chunks), kPlaneWarps * 32, smem, st>>>(
         rows, rcnt, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-        (int)g.tiles, g.cap, chunks, entries, offs);
+        (int)g.tiles, g.cap, chunks, entries, offs, Gate{});
     return cudaGetLastError();
 }
 

@@ -44,6 +44,7 @@ struct Args {
     int K, Kg, Cg, R, S, T, P, Ho, Wo, HoWo, relu;
     int rows, ptiles, mtiles, cb, kblocks, npix, nmma;
     uint32_t idesc;
+    Gate gate;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -93,7 +94,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 
 // in [N][C][H*W] -> nhwc [N][H*W][Cp], TF32-rounded (RNA); channels >= C are 0.
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                          int C, int Cp, int HW) {
+                                                          int C, int Cp, int HW, Gate gate) {
+    if (gate_closed(gate)) return;
     __shared__ float tile[32][33];
     const int n = blockIdx.z;
     const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
 }
 
 __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ CUtensorMap bmap, const Args a) {
+    if (gate_closed(a.gate)) return;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128 atoms
     unsigned char* sA = smem;                                  // STAGES x 16 KB
@@ -336,12 +339,13 @@ cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float
 }
 
 cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, float* nhwc,
-                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st) {
+                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st,
+                            Gate gate) {
     using namespace dense;
     if (!dg.supported) return cudaErrorNotSupported;
     const int HW = (int)(g.H * g.W);
     dim3 tgrid((unsigned)((HW + 31) / 32), (unsigned)((dg.cp + 31) / 32), (unsigned)n);
-    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, HW);
+    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, HW, gate);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     Args a;
@@ -351,6 +355,7 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     a.K = (int)g.K; a.Kg = (int)g.Kg; a.Cg = (int)g.Cg; a.R = (int)g.R; a.S = (int)g.S;
     a.T = (int)g.T; a.P = (int)g.P; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo; a.HoWo = (int)(g.Ho * g.Wo);
     a.relu = g.relu ? 1 : 0;
+    a.gate = gate;
     a.rows = (int)dg.rows; a.ptiles = (int)dg.ptiles; a.mtiles = (int)dg.mtiles; a.cb = (int)dg.cb;
     a.kblocks = (int)dg.kblocks; a.npix = (int)dg.npix; a.nmma = (int)dg.nmma;
     // instruction descriptor: D f32 [4,6)=1, A tf32 [7,10)=2, B tf32 [10,13)=2, both K-major,

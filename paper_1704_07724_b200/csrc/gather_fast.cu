@@ -13,7 +13,7 @@ bool matches(const Geometry& g) {
 #define SC_DECLARE(VV)                                                                                  \
     cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,   \
                             const float* wpack, const float* bias, float* out, uint2* rowlist,          \
-                            uint32_t* rowcnt, cudaStream_t st);
+                            uint32_t* rowcnt, cudaStream_t st, Gate gate);
 SC_GATHER_VARIANTS(SC_DECLARE)
 #undef SC_DECLARE
 }  // namespace fast
@@ -48,10 +48,10 @@ bool gather_fast_can_emit(int variant) {
 
 cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
                                const float* wpack, const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt,
-                               cudaStream_t st) {
+                               cudaStream_t st, Gate gate) {
     using namespace fast;
 #define SC_LAUNCH(VV) \
-    if (variant == VV::ID) return launch_##VV(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st);
+    if (variant == VV::ID) return launch_##VV(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st, gate);
     SC_GATHER_VARIANTS(SC_LAUNCH)
 #undef SC_LAUNCH
     return cudaErrorInvalidValue;

@@ -51,6 +51,7 @@ struct Args {
     int n, C, H, K, Cg, Kg, kblocks, Ho, relu;
     int64_t cap;
     int ytiles, units, ctas_per_kb;
+    Gate gate;  // f3: device-side path selection
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     using SM = Smem<V>;
     constexpr int RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO;
     constexpr int CH = V::CH, STAGES = V::STAGES, NW = V::NW, KBW = SM::KBW;
+    if (gate_closed(a.gate)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring);
@@ -353,12 +355,13 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
 
 template <class V>
 cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs, const float* wpack,
-                     const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt, cudaStream_t st) {
+                     const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt, cudaStream_t st, Gate gate) {
     if (g.ty != V::TY || g.tiles != (g.Ho + V::TY - 1) / V::TY || (g.Cg + V::CH - 1) / V::CH > 63)
         return cudaErrorInvalidValue;
     Args a;
     a.entries = entries; a.offs = offs; a.wpack = wpack; a.bias = bias; a.out = out;
     a.rowlist = rowlist; a.rowcnt = rowcnt;
+    a.gate = gate;
     a.n = (int)n; a.C = (int)g.C; a.H = (int)g.H; a.K = (int)g.K; a.Cg = (int)g.Cg; a.Kg = (int)g.Kg;
     a.kblocks = (int)g.kblocks; a.Ho = (int)g.Ho; a.relu = g.relu ? 1 : 0;
     a.cap = g.cap;
@@ -390,8 +393,8 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     namespace fast {                                                                                        \
     cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,       \
                             const float* wpack, const float* bias, float* out, uint2* rowlist,              \
-                            uint32_t* rowcnt, cudaStream_t st) {                                            \
-        return launch_v<VV>(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st);                    \
+                            uint32_t* rowcnt, cudaStream_t st, Gate gate) {                                 \
+        return launch_v<VV>(g, n, entries, offs, wpack, bias, out, rowlist, rowcnt, st, gate);              \
     }                                                                                                       \
     }                                                                                                       \
     }

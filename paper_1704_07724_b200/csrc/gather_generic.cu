@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
     const uint2* __restrict__ entries, const uint32_t* __restrict__ offs, const float* __restrict__ wpack,
     const float* __restrict__ bias, float* __restrict__ out, int64_t total_warps, int64_t C, int64_t H, int64_t W,
     int64_t K, int64_t R, int64_t S, int64_t T, int64_t P, int64_t Cg, int64_t Kg, int64_t Kg_pad, int64_t kbw,
-    int64_t Ho, int64_t Wo, int64_t cap, int relu) {
+    int64_t Ho, int64_t Wo, int64_t cap, int relu, Gate gate) {
+    if (gate_closed(gate)) return;
     __shared__ float acc_s[8][32][33];
     const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     int64_t wid = (int64_t)blockIdx.x * 8 + wib;
@@ -81,13 +82,14 @@ __global__ void __launch_bounds__(256) gather_generic_kernel(
 }
 
 cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
-                                  const float* wpack, const float* bias, float* out, cudaStream_t st) {
+                                  const float* wpack, const float* bias, float* out, cudaStream_t st,
+                                  Gate gate) {
     if (g.tiles != 1) return cudaErrorInvalidValue;  // generic path runs on one tile per image
     const int64_t total_warps = n * g.G * (g.Kg_pad / 32) * g.Ho * ((g.Wo + 31) / 32);
     const int64_t blocks = (total_warps + 7) / 8;
     gather_generic_kernel<<<(unsigned)blocks, 256, 0, st>>>(entries, offs, wpack, bias, out, total_warps, g.C, g.H,
                                                             g.W, g.K, g.R, g.S, g.T, g.P, g.Cg, g.Kg, g.Kg_pad,
-                                                            g.kbw, g.Ho, g.Wo, g.cap, g.relu ? 1 : 0);
+                                                            g.kbw, g.Ho, g.Wo, g.cap, g.relu ? 1 : 0, gate);
     return cudaGetLastError();
 }
 

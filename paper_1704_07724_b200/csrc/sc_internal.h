@@ -9,6 +9,16 @@
 
 namespace sc {
 
+// Device-side path selection: a kernel launched with a gate
+// returns at once unless *flag == run_if (flag null: always runs).  Lets the
+// sparse and the dense path both be enqueued (graph-capturable) while only the
+// one chosen on the device from the batch's measured density does work.
+struct Gate {
+    const int* flag = nullptr;
+    int run_if = 0;
+};
+__device__ __forceinline__ bool gate_closed(const Gate& g) { return g.flag != nullptr && *g.flag != g.run_if; }
+
 // Geometry derived once at plan creation.
 struct Geometry {
     int64_t N, C, H, W, K, R, S, T, P, G;
@@ -43,13 +53,14 @@ cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float
 // prow [N*C][H+1] u32; they may be null otherwise.
 bool compact_uses_counts(const Geometry& g);
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
-                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st);
+                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate = {});
 // Stage 1 of a chained consumer (f1): the producing gather wrote per-(plane, row)
 // lists `rows` [N*C*H][W] and counts `rcnt` [N*C*H]; builds the same R9 streams.
 cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt, const uint2* rows,
                                      const uint32_t* rcnt, uint2* entries, uint32_t* offs, cudaStream_t st);
 cudaError_t launch_gather_generic(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,
-                                  const float* wpack, const float* bias, float* out, cudaStream_t st);
+                                  const float* wpack, const float* bias, float* out, cudaStream_t st,
+                                  Gate gate = {});
 
 // Shape-specialised stage-2 kernels (gather_fast.cu).  `select` returns a
 // variant id > 0 (and its lanes-per-channel KL and tile height TY) if one
@@ -60,11 +71,20 @@ bool gather_fast_can_emit(int variant);  // the variant can emit chained lists (
 // out may then be null.  cudaErrorNotSupported if the variant cannot emit.
 cudaError_t launch_gather_fast(int variant, const Geometry& g, int64_t n, const uint2* entries,
                                const uint32_t* offs, const float* wpack, const float* bias, float* out,
-                               uint2* rowlist, uint32_t* rowcnt, cudaStream_t st);
+                               uint2* rowlist, uint32_t* rowcnt, cudaStream_t st, Gate gate = {});
 
 // Dense tcgen05 TF32 implicit GEMM (dense_tc.cu).
 cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, const float* in, float* nhwc,
-                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st);
+                            const void* map128, const float* wdense, const float* bias, float* out, cudaStream_t st,
+                            Gate gate = {});
+
+// f3 path selection (select.cu).  sel: 4 x u64 device words (nnz, ticket,
+// path flag, last nnz), zero-initialised; the kernel leaves nnz/ticket at 0.
+constexpr int kPathSparse = 0;
+constexpr int kPathDense = 1;
+cudaError_t launch_select_path(const float* in, int64_t elems, unsigned long long thr, unsigned long long* sel,
+                               cudaStream_t st);
+cudaError_t launch_synth_relu(float* x, int64_t elems, double rho, uint32_t seed, cudaStream_t st);
 
 cudaError_t probe_fma(int kind, double* rate);
 cudaError_t launch_flush(void* scratch, size_t bytes, cudaStream_t st);

@@ -22,7 +22,10 @@ STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_SHAPE", 3: "SC_ER
 EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forward", "dense_conv_forward",
            "sparse_conv_forward_host", "sparse_conv_destroy", "sc_status_string", "sc_last_error",
            "sparse_conv_compact", "sparse_conv_gather", "sparse_conv_lists", "sparse_conv_kernel_variant",
-           "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain")
+           "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
+           "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
+           "sparse_conv_get_crossover", "sparse_conv_last_path")
+SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
 class SparseConvError(RuntimeError):
@@ -56,7 +59,7 @@ def lib():
         vp, i64, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
         L.sparse_conv_output_shape.argtypes = [ctypes.POINTER(ConvParams), ctypes.POINTER(ctypes.c_int64)]
         L.sparse_conv_create.argtypes = [ctypes.POINTER(ConvParams), vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
-        for fn in ("sparse_conv_forward", "dense_conv_forward", "sparse_conv_forward_host"):
+        for fn in ("sparse_conv_forward", "dense_conv_forward", "sparse_conv_forward_host", "sparse_conv_forward_auto"):
             getattr(L, fn).argtypes = [vp, i64, vp, vp, vp]
         L.sparse_conv_compact.argtypes = [vp, i64, vp, vp]
         L.sparse_conv_forward_chain.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64, vp, ctypes.POINTER(vp), vp]
@@ -65,6 +68,10 @@ def lib():
         L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
         L.sparse_conv_kernel_variant.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_char_p)]
         L.sparse_conv_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+        L.sparse_conv_calibrate_crossover.argtypes = [vp, i64, vp, ctypes.POINTER(ctypes.c_double)]
+        L.sparse_conv_set_crossover.argtypes = [vp, ctypes.c_double]
+        L.sparse_conv_get_crossover.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+        L.sparse_conv_last_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]
         L.sc_probe_fma.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
         L.sc_flush_l2.argtypes = [vp, ctypes.c_size_t, vp]
         L.sc_status_string.argtypes = [st]
@@ -157,6 +164,41 @@ class SparseConv:
         _check(lib().dense_conv_forward(self._plan, n, ctypes.c_void_p(x.data_ptr()),
                                         ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
         return out
+
+    def forward_auto(self, x, out=None, stream=None):
+        """Sparse or dense path, chosen on the device from x's sparsity (f3)."""
+        n = x.shape[0]
+        _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+        if out is None:
+            out = torch.empty((n,) + self.out_shape, device=self.device, dtype=torch.float32)
+        _check_tensor(out, "out", self.device, (n,) + self.out_shape)
+        _check(lib().sparse_conv_forward_auto(self._plan, n, ctypes.c_void_p(x.data_ptr()),
+                                              ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def calibrate_crossover(self, n, stream=None):
+        """Measure the crossover sparsity s* for batches of n; returns it."""
+        v = ctypes.c_double()
+        with torch.cuda.device(self.device):
+            _check(lib().sparse_conv_calibrate_crossover(self._plan, n, _stream_handle(stream), ctypes.byref(v)))
+        return v.value
+
+    @property
+    def crossover(self):
+        """s*: forward_auto takes the sparse path iff the batch sparsity >= s* (None: not set)."""
+        v = ctypes.c_double()
+        _check(lib().sparse_conv_get_crossover(self._plan, ctypes.byref(v)))
+        return None if v.value < 0 else v.value
+
+    @crossover.setter
+    def crossover(self, s_star):
+        _check(lib().sparse_conv_set_crossover(self._plan, float(s_star)))
+
+    def last_path(self):
+        """(path, nnz) of the last forward_auto: path SC_PATH_SPARSE (0) or SC_PATH_DENSE (1)."""
+        p, z = ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().sparse_conv_last_path(self._plan, ctypes.byref(p), ctypes.byref(z)))
+        return p.value, z.value
 
     def forward_host(self, h_in, h_out, stream=None):
         """End-to-end call with HOST (ideally pinned) CPU tensors."""
