@@ -25,6 +25,9 @@ exact_nonzero_macs  P:121 (Sec. 4) "MACs can be reduce to rho*...": the exact
                     the inverse map of P:121 with divisibility/range guards (R6)
 estimated_macs      P:121: round(rho * dense_macs)
 sparsity            P:121: 1 - #nonzeros / size
+conv_backward_fp64  SURVEY 8f row f4 (training): weight gradient,
+                    bias gradient and the input gradient through the producing
+                    ReLU (Eq. 2), R19-R20.  (C, OpenMP)
 
 Parity status: every function above is pinned by tests/test_oracle.py (brute
 force with exact rationals, torch conv2d float64, closed forms, invariants,
@@ -62,6 +65,8 @@ def _load():
         vp = ctypes.c_void_p
         lib.oracle_conv_fp64.restype = ctypes.c_int
         lib.oracle_conv_fp64.argtypes = [vp, vp, vp] + [i64] * 10 + [vp, vp]
+        lib.oracle_conv_backward_fp64.restype = ctypes.c_int
+        lib.oracle_conv_backward_fp64.argtypes = [vp, vp, vp] + [i64] * 10 + [vp] * 5
         lib.oracle_compact_streams.restype = ctypes.c_int
         lib.oracle_compact_streams.argtypes = [vp] + [i64] * 10 + [vp, vp]
         _lib = lib
@@ -158,6 +163,38 @@ def conv_fp64(x, w, bias=None, stride=1, pad=0, groups=1, want_mass=True):
     if rc != 0:
         raise ValueError("oracle_conv_fp64: invalid shape")
     return out, mass
+
+
+def conv_backward_fp64(x, w, dout, stride=1, pad=0, groups=1, want_mass=True):
+    """Gradients of Eq. 1 (R19-R20), in double.
+
+    dw[k,c,r,t] = sum_{n,y,x} in[n,c,yT+r-P,xT+t-P] * dout[n,k,y,x]
+    dbias[k]    = sum_{n,y,x} dout[n,k,y,x]
+    dz[n,c,i,j] = [in != 0] * sum_{k,r,t} W[k,c,r,t] * dout[n,k,(i+P-r)/T,(j+P-t)/T]
+                  (terms with a non-integral or out-of-range output index dropped)
+    dz is the gradient through the ReLU that produced `in` (Eq. 2).  Returns
+    dict(dw, dw_mass, dbias, dz, dz_mass) of float64 arrays (masses None if not
+    requested)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    dout = np.ascontiguousarray(dout, dtype=np.float32)
+    n, c, h, ww = x.shape
+    k, cg, r, s = w.shape
+    if cg * groups != c:
+        raise ValueError("weight shape does not match C/groups")
+    shp = output_shape(n, c, h, ww, k, r, s, stride, pad, groups)
+    if dout.shape != shp:
+        raise ValueError(f"dout shape {dout.shape} != output shape {shp}")
+    dw = np.empty(w.shape, np.float64)
+    dbias = np.empty(k, np.float64)
+    dz = np.empty(x.shape, np.float64)
+    dwm = np.empty(w.shape, np.float64) if want_mass else None
+    dzm = np.empty(x.shape, np.float64) if want_mass else None
+    rc = _load().oracle_conv_backward_fp64(_ptr(x), _ptr(w), _ptr(dout), n, c, h, ww, k, r, s, stride, pad,
+                                           groups, _ptr(dw), _ptr(dwm), _ptr(dbias), _ptr(dz), _ptr(dzm))
+    if rc != 0:
+        raise ValueError("oracle_conv_backward_fp64: invalid shape")
+    return dict(dw=dw, dw_mass=dwm, dbias=dbias, dz=dz, dz_mass=dzm)
 
 
 # --------------------------------------------------------------------------

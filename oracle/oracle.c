@@ -21,6 +21,11 @@
  *                        zero elements of the input data, and store the
  *                        non-zero values in a vector with their column and row
  *                        information", in the tile-stream format of DESIGN.md R9.
+ *   oracle_conv_backward_fp64 -- SURVEY 8f row f4: the gradients of Eq. 1
+ *                        (chain rule) for training, where the paper measures
+ *                        the sparsity (Sec. 1; Sec. 3);
+ *                        the input-gradient is taken through the producing
+ *                        ReLU (Eq. 2), R19-R20.
  *
  * Build: gcc -O2 -fopenmp -fPIC -shared (no -ffast-math: rounding and IEEE
  * zero tests must be exact).
@@ -159,4 +164,118 @@ int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int
         }
     }
     return bad ? -1 : 0;
+}
+
+/*
+ * Backward of Eq. 1 (R19, R20).  With out = conv(in, W) + bias and
+ * the upstream gradient dout = dL/dout [N][K][Ho][Wo]:
+ *
+ *   dw[k][cl][r][t] = sum_{n,y,x} in[n, g*Cg+cl, y*T+r-P, x*T+t-P] * dout[n,k,y,x]
+ *                     (g = k / Kg; reads outside the plane are zero)
+ *   dbias[k]        = sum_{n,y,x} dout[n,k,y,x]
+ *   dz[n][c][i][j]  = [in[n,c,i,j] != 0] *
+ *                     sum_{k in group(c)} sum_{r,t : y = (i+P-r)/T, x = (j+P-t)/T
+ *                                          integral and in range} W[k][cl][r][t] * dout[n,k,y,x]
+ *
+ * dz is dL/dz for in = ReLU(z) (Eq. 2: the derivative is 1 where the ReLU
+ * output is positive, 0 elsewhere; for a ReLU output in != 0 <=> in > 0).
+ * Accumulation in double; the loop orders are the definitions' (k,cl,r,t |
+ * n,y,x) and (n,c,i,j | k,r,t).  dw_mass / dz_mass (nullable) are the sums of
+ * the absolute values of the same products (tolerance scales).
+ * in, dout: float; w: float [K][Cg][R][S]; outputs double.
+ * Returns 0, or -1 on invalid shape.
+ */
+int oracle_conv_backward_fp64(const float *in, const float *w, const float *dout,
+                              int64_t N, int64_t C, int64_t H, int64_t W,
+                              int64_t K, int64_t R, int64_t S,
+                              int64_t stride, int64_t pad, int64_t groups,
+                              double *dw, double *dw_mass, double *dbias,
+                              double *dz, double *dz_mass)
+{
+    if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || R < 1 || S < 1 ||
+        stride < 1 || pad < 0 || groups < 1 || C % groups || K % groups)
+        return -1;
+    if (R > H + 2 * pad || S > W + 2 * pad) return -1;
+    const int64_t Ho = out_extent(H, pad, R, stride);
+    const int64_t Wo = out_extent(W, pad, S, stride);
+    const int64_t Cg = C / groups, Kg = K / groups;
+    const int64_t T = stride, P = pad;
+
+    if (dw) {
+        #pragma omp parallel for collapse(2) schedule(static)
+        for (int64_t k = 0; k < K; ++k) {
+            for (int64_t cl = 0; cl < Cg; ++cl) {
+                const int64_t c = (k / Kg) * Cg + cl;
+                for (int64_t r = 0; r < R; ++r) {
+                    for (int64_t t = 0; t < S; ++t) {
+                        double acc = 0.0, m = 0.0;
+                        for (int64_t n = 0; n < N; ++n) {
+                            for (int64_t y = 0; y < Ho; ++y) {
+                                const int64_t i = y * T + r - P;
+                                if (i < 0 || i >= H) continue;
+                                for (int64_t x = 0; x < Wo; ++x) {
+                                    const int64_t j = x * T + t - P;
+                                    if (j < 0 || j >= W) continue;
+                                    const double v = (double)in[((n * C + c) * H + i) * W + j];
+                                    const double d = (double)dout[((n * K + k) * Ho + y) * Wo + x];
+                                    acc += v * d;
+                                    m += fabs(v) * fabs(d);
+                                }
+                            }
+                        }
+                        const int64_t o = ((k * Cg + cl) * R + r) * S + t;
+                        dw[o] = acc;
+                        if (dw_mass) dw_mass[o] = m;
+                    }
+                }
+            }
+        }
+    }
+    if (dbias) {
+        for (int64_t k = 0; k < K; ++k) {
+            double acc = 0.0;
+            for (int64_t n = 0; n < N; ++n)
+                for (int64_t y = 0; y < Ho; ++y)
+                    for (int64_t x = 0; x < Wo; ++x)
+                        acc += (double)dout[((n * K + k) * Ho + y) * Wo + x];
+            dbias[k] = acc;
+        }
+    }
+    if (dz) {
+        #pragma omp parallel for collapse(2) schedule(static)
+        for (int64_t n = 0; n < N; ++n) {
+            for (int64_t c = 0; c < C; ++c) {
+                const int64_t g = c / Cg, cl = c - g * Cg;
+                for (int64_t i = 0; i < H; ++i) {
+                    for (int64_t j = 0; j < W; ++j) {
+                        const int64_t o = ((n * C + c) * H + i) * W + j;
+                        double acc = 0.0, m = 0.0;
+                        if (in[o] != 0.0f) {
+                            for (int64_t k = g * Kg; k < (g + 1) * Kg; ++k) {
+                                for (int64_t r = 0; r < R; ++r) {
+                                    const int64_t yT = i + P - r;
+                                    if (yT < 0 || yT % T) continue;
+                                    const int64_t y = yT / T;
+                                    if (y >= Ho) continue;
+                                    for (int64_t t = 0; t < S; ++t) {
+                                        const int64_t xT = j + P - t;
+                                        if (xT < 0 || xT % T) continue;
+                                        const int64_t x = xT / T;
+                                        if (x >= Wo) continue;
+                                        const double wt = (double)w[((k * Cg + cl) * R + r) * S + t];
+                                        const double d = (double)dout[((n * K + k) * Ho + y) * Wo + x];
+                                        acc += wt * d;
+                                        m += fabs(wt) * fabs(d);
+                                    }
+                                }
+                            }
+                        }
+                        dz[o] = acc;
+                        if (dz_mass) dz_mass[o] = m;
+                    }
+                }
+            }
+        }
+    }
+    return 0;
 }
