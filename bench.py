@@ -29,6 +29,7 @@ data); C5: the 1024-image batch is sharded.  No collective on the data path
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -593,6 +594,71 @@ def run_table2(args):
     return 0
 
 
+def run_backward(args):
+    """sparse_conv_backward (plane lists + wgrad + split reduce + dbias +
+    ReLU-masked dgrad) on the workload's batch at several sparsities, graph-timed, with
+    the library dense backward (cuDNN via torch autograd, TF32 allowed and not) as context."""
+    import torch
+    from paper_1704_07724_b200 import sparseconv as sc
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    shp = datagen.CONFIGS[args.config]
+    n = shp.n
+    w, b = datagen.weights(shp)
+    wd = torch.from_numpy(w).to(dev)
+    conv = sc.SparseConv(wd, torch.from_numpy(b).to(dev), n, shp.c, shp.h, shp.w, shp.stride, shp.pad, shp.groups)
+    d = torch.from_numpy(np.random.default_rng(31).standard_normal((n, shp.k, shp.ho, shp.wo)).astype(np.float32))
+    d = d.to(dev)
+    out_dw = torch.empty_like(wd)
+    out_db = torch.empty(shp.k, device=dev)
+    out_dz = torch.empty((n, shp.c, shp.h, shp.w), device=dev)
+    L = sc.lib()
+    def ptr(t):
+        return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+    def bwd(x, dw=out_dw, db=out_db, dz=out_dz):
+        sc._check(L.sparse_conv_backward(conv._plan, n, ptr(x), ptr(d), ptr(dw), ptr(db), ptr(dz),
+                                         sc._stream_handle(stream)))
+
+    def cudnn(x, tf32):
+        torch.backends.cudnn.allow_tf32 = tf32
+        xr = x.clone().requires_grad_(True)
+        wr = wd.clone().requires_grad_(True)
+        br = torch.zeros(shp.k, device=dev, requires_grad=True)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                o = torch.nn.functional.conv2d(xr, wr, br, stride=shp.stride, padding=shp.pad, groups=shp.groups)
+                o.backward(d)
+            stream.synchronize()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                o = torch.nn.functional.conv2d(xr, wr, br, stride=shp.stride, padding=shp.pad, groups=shp.groups)
+                o.backward(d)
+            e.record(stream)
+            e.synchronize()
+        return a.elapsed_time(e) * 1e3 / 10  # includes the forward: an upper bound on the backward alone
+
+    rows = {}
+    for s in (0.9, 0.95, 0.99):
+        x = torch.from_numpy(datagen.activations(shp, s)).to(dev)
+        dense, exact, nnz = mac_counts(x, shp)
+        t_all = graph_time_us(torch, stream, lambda: bwd(x), reps=10)
+        t_w = graph_time_us(torch, stream, lambda: bwd(x, db=None, dz=None), reps=10)
+        t_z = graph_time_us(torch, stream, lambda: bwd(x, dw=None, db=None), reps=10)
+        flops = 2 * 2 * exact  # wgrad and dgrad each run the exact nonzero MACs
+        rows[str(s)] = {"us": round(t_all, 2), "wgrad_us": round(t_w, 2), "dgrad_us": round(t_z, 2),
+                        "nonzero_tflops": round(flops / (t_all * 1e-6) / 1e12, 3),
+                        "frac_fp32": round(flops / (t_all * 1e-6) / 1e12 / FP32_PEAK_TFLOPS, 4),
+                        "cudnn_fwd_bwd_tf32_us": round(cudnn(x, True), 2),
+                        "cudnn_fwd_bwd_fp32_us": round(cudnn(x, False), 2)}
+    torch.backends.cudnn.allow_tf32 = True
+    print(json.dumps({"backward": rows, "workload": workload_name(shp, args.sparsity, n), "data": "synthetic",
+                      "note": "sparse_conv_backward (dw, dbias, ReLU-masked dz) graph-timed, L2-warm; cudnn_* = "
+                              "torch conv2d forward+backward (dw, db, dx) per step, context only"}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -605,7 +671,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--table2", action="store_true", help="paper Table 2 layers: sparse vs dense on B200")
     ap.add_argument("--table2-batch", type=int, default=128)
+    ap.add_argument("--backward", action="store_true", help="f4: sparse backward vs library dense backward")
     args = ap.parse_args()
+    if args.backward:
+        return run_backward(args)
     if args.table2:
         return run_table2(args)
     if args.warmup < 3:

@@ -191,6 +191,29 @@ sc_status sparse_conv_get_crossover(sc_plan plan, double *s_star);
  * Synchronizes the device. */
 sc_status sparse_conv_last_path(sc_plan plan, int32_t *path, int64_t *nnz);
 
+/* ---- backward with sparse activations ------------------
+ * The paper measures the ReLU sparsity during training but gives
+ * no backward algorithm; this is the chain rule of Eq. 1 (R19-R20)
+ * for the first n images, skipping zero inputs:
+ *   d_dw    [K][C/G][R][S]  dW[k,c,r,t] = sum_{n,y,x} in[n,c,yT+r-P,xT+t-P] * dout[n,k,y,x]
+ *   d_dbias [K]             sum_{n,y,x} dout[n,k,y,x]
+ *   d_dz    [n][C][H][W]    dz[n,c,i,j] = [in[n,c,i,j] != 0] *
+ *                               sum_{k,r,t} W[k,c,r,t] * dout[n,k,(i+P-r)/T,(j+P-t)/T]
+ *                           (terms with a non-integral or out-of-range output index dropped):
+ *                           the gradient through the ReLU that produced `in` (Eq. 2), zero
+ *                           wherever in == 0.
+ * d_in is the forward input [n][C][H][W], d_dout the gradient of this layer's
+ * convolution output [n][K][H_out][W_out] (if the plan fuses a ReLU on its
+ * output, pass the gradient w.r.t. the pre-ReLU output).  d_dw, d_dbias, d_dz
+ * are caller-owned outputs, each nullable (not computed), fully overwritten.
+ * fp32 accumulation in a fixed order (deterministic).  Stream-ordered, no
+ * allocation, graph-capturable; shares the plan's list workspace with the
+ * forward (do not overlap the two).  SC_ERR_UNSUPPORTED unless the plan uses
+ * the plane-major stage 1 (H*W <= 1024, H <= 31, <= 32 row tiles) and R x S is
+ * 1x1, 3x3 or 5x5. */
+sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float *d_in, const float *d_dout, float *d_dw,
+                               float *d_dbias, float *d_dz, sc_stream_t stream);
+
 /* Free everything the plan owns.  NULL is a no-op. */
 sc_status sparse_conv_destroy(sc_plan plan);
 

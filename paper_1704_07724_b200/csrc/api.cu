@@ -11,6 +11,7 @@
 
 #include "sc_internal.h"
 
+using sc::BwdGeom;
 using sc::DenseGeom;
 using sc::Geometry;
 
@@ -19,6 +20,8 @@ struct sc_plan_s {
     int device;
     Geometry g;
     DenseGeom dg;
+    BwdGeom bg;
+    float* bws = nullptr;      // backward: wgrad partials [splits_w][K][Cg][R][S]
     float* wpack = nullptr;    // [G][Kg_pad/kbw][Cg][R][S][kbw] (pack.cu)
     float* wdense = nullptr;   // dense path A operand [G][mtiles][kblocks][128x32], TF32, swizzled
     float* nhwc = nullptr;     // dense path: channels-last TF32 copy of the input [N][H][W][Cp]
@@ -164,6 +167,7 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
     cudaFree(p->sel);
+    cudaFree(p->bws);
     delete p;
 }
 
@@ -298,6 +302,7 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     }
     const Geometry& g = plan->g;
     const DenseGeom& dg = plan->dg;
+    sc::backward_geometry(g, &plan->bg);
     cudaError_t e;
     const size_t wbytes = sizeof(float) * g.G * g.Cg * g.R * g.S * g.Kg_pad;
     const size_t dbytes = sizeof(float) * sc::dense_workspace_floats(g, dg);
@@ -309,6 +314,8 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         (e = cudaMalloc(&plan->entries, sizeof(uint2) * (g.N * g.tiles * g.cap + 2))) != cudaSuccess ||
         (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess ||
         (e = cudaMalloc(&plan->sel, 4 * sizeof(unsigned long long))) != cudaSuccess ||
+        (plan->bg.supported &&
+         (e = cudaMalloc(&plan->bws, sizeof(float) * plan->bg.splits_w * g.K * g.Cg * g.R * g.S)) != cudaSuccess) ||
         (sc::compact_uses_counts(g) &&
          ((e = cudaMalloc(&plan->cnt, sizeof(uint32_t) * g.N * g.tiles * g.C)) != cudaSuccess ||
           (e = cudaMalloc(&plan->plist, sizeof(uint2) * g.N * g.C * g.H * g.W)) != cudaSuccess ||
@@ -563,6 +570,29 @@ sc_status sparse_conv_last_path(sc_plan plan, int32_t* path, int64_t* nnz) {
     if (path) *path = (int32_t)(h[2] & 0xffffffffu);
     if (nnz) *nnz = (int64_t)h[3];
     return SC_OK;
+}
+
+sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float* d_in, const float* d_dout, float* d_dw,
+                               float* d_dbias, float* d_dz, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if (!plan->bg.supported)
+        return fail(SC_ERR_UNSUPPORTED, "backward: needs a plane-major plan (H*W <= 1024, H <= 31, tiles <= 32) "
+                                        "and a 1x1, 3x3 or 5x5 kernel");
+    if ((st = check_dev_ptr(plan, d_in, "d_in")) != SC_OK || (st = check_dev_ptr(plan, d_dout, "d_dout")) != SC_OK)
+        return st;
+    if ((d_dw && (st = check_dev_ptr(plan, d_dw, "d_dw")) != SC_OK) ||
+        (d_dbias && (st = check_dev_ptr(plan, d_dbias, "d_dbias")) != SC_OK) ||
+        (d_dz && (st = check_dev_ptr(plan, d_dz, "d_dz")) != SC_OK))
+        return st;
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (d_dw || d_dz) e = sc::launch_plane_lists(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, s);
+    if (e == cudaSuccess)
+        e = sc::launch_backward(plan->g, plan->bg, n, plan->plist, plan->prow, d_dout, plan->wpack, plan->bws, d_dw,
+                                d_dbias, d_dz, s);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "backward launch");
 }
 
 sc_status sparse_conv_lists(sc_plan plan, sc_lists_view* out) {

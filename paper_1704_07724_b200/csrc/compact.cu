@@ -430,10 +430,10 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     }
 }
 
-cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
-                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate) {
+cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
+                               uint32_t* prow, cudaStream_t st, Gate gate) {
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
-        return launch_compact_streamwise(g, n, in, entries, offs, st, gate);
+        return cudaErrorNotSupported;
     const int TYT = (int)(g.ty * g.T);
     const int planes = (int)(n * g.C);
     const unsigned cgrid = (unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps);
@@ -451,7 +451,14 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     else if (slots <= 25) SC_COUNT(25);
     else SC_COUNT(kMaxSlots);
 #undef SC_COUNT
-    cudaError_t e = cudaGetLastError();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
+                           uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate) {
+    if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
+        return launch_compact_streamwise(g, n, in, entries, offs, st, gate);
+    cudaError_t e = launch_plane_lists(g, n, in, cnt, plist, prow, st, gate);
     if (e != cudaSuccess) return e;
     const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
     compact_plane_emit_kernel<false><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(

@@ -40,6 +40,16 @@ struct DenseGeom {
     bool supported;
 };
 
+// Backward kernels (backward.cu): KC = 32*kl output channels
+// per warp pass, kchunks per group, cblocks of 16 channels, bands of `by` output
+// rows staged in shared memory (smem bytes), image splits for wgrad / dgrad.
+struct BwdGeom {
+    int64_t kl, kc, kchunks, cblocks, by, bands, splits_w, splits_d, tile_floats;
+    size_t smem;
+    bool bulk;  // dout tiles by one TMA bulk copy each, double buffered
+    bool supported;
+};
+
 // ---- kernels (launchers return cudaGetLastError()) -------------------------
 cudaError_t launch_pack_weights(const Geometry& g, const float* w, float* wpack, cudaStream_t st);
 void dense_geometry(const Geometry& g, DenseGeom* dg);
@@ -54,6 +64,10 @@ cudaError_t encode_dense_input_map(const Geometry& g, const DenseGeom& dg, float
 bool compact_uses_counts(const Geometry& g);
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
                            uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate = {});
+// Only the plane lists plist/prow (and tile counts cnt) of the plane-major path;
+// cudaErrorNotSupported unless compact_uses_counts(g).
+cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
+                               uint32_t* prow, cudaStream_t st, Gate gate = {});
 // Stage 1 of a chained consumer (f1): the producing gather wrote per-(plane, row)
 // lists `rows` [N*C*H][W] and counts `rcnt` [N*C*H]; builds the same R9 streams.
 cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt, const uint2* rows,
@@ -85,6 +99,12 @@ constexpr int kPathDense = 1;
 cudaError_t launch_select_path(const float* in, int64_t elems, unsigned long long thr, unsigned long long* sel,
                                cudaStream_t st);
 cudaError_t launch_synth_relu(float* x, int64_t elems, double rho, uint32_t seed, cudaStream_t st);
+
+// Backward (backward.cu).  ws: [splits_w][K][Cg][R][S] floats.  dw/dbias/dz nullable.
+void backward_geometry(const Geometry& g, BwdGeom* b);
+cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, const uint2* plist, const uint32_t* prow,
+                            const float* dout, const float* wpack, float* ws, float* dw, float* dbias, float* dz,
+                            cudaStream_t st);
 
 cudaError_t probe_fma(int kind, double* rate);
 cudaError_t launch_flush(void* scratch, size_t bytes, cudaStream_t st);

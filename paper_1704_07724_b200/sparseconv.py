@@ -24,7 +24,7 @@ EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forwar
            "sparse_conv_compact", "sparse_conv_gather", "sparse_conv_lists", "sparse_conv_kernel_variant",
            "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
            "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
-           "sparse_conv_get_crossover", "sparse_conv_last_path")
+           "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward")
 SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
@@ -68,6 +68,7 @@ def lib():
         L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
         L.sparse_conv_kernel_variant.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_char_p)]
         L.sparse_conv_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+        L.sparse_conv_backward.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
         L.sparse_conv_calibrate_crossover.argtypes = [vp, i64, vp, ctypes.POINTER(ctypes.c_double)]
         L.sparse_conv_set_crossover.argtypes = [vp, ctypes.c_double]
         L.sparse_conv_get_crossover.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
@@ -199,6 +200,26 @@ class SparseConv:
         p, z = ctypes.c_int32(), ctypes.c_int64()
         _check(lib().sparse_conv_last_path(self._plan, ctypes.byref(p), ctypes.byref(z)))
         return p.value, z.value
+
+    def backward(self, x, dout, want_dw=True, want_dbias=True, want_dz=True, stream=None):
+        """Gradients of the convolution skipping zero inputs (f4): returns
+        (dw [K][C/G][R][S], dbias [K], dz [n][C][H][W]) -- dz is the input
+        gradient through the ReLU that produced x (zero where x == 0); an
+        output not wanted is None."""
+        n = x.shape[0]
+        _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+        _check_tensor(dout, "dout", self.device, (n,) + self.out_shape)
+        p = self.params
+        dw = torch.empty((p.k, p.c // p.groups, p.r, p.s), device=self.device) if want_dw else None
+        db = torch.empty((p.k,), device=self.device) if want_dbias else None
+        dz = torch.empty_like(x) if want_dz else None
+
+        def ptr(t):
+            return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+        _check(lib().sparse_conv_backward(self._plan, n, ptr(x), ptr(dout), ptr(dw), ptr(db), ptr(dz),
+                                          _stream_handle(stream)))
+        return dw, db, dz
 
     def forward_host(self, h_in, h_out, stream=None):
         """End-to-end call with HOST (ideally pinned) CPU tensors."""
