@@ -30,6 +30,8 @@
 //    optional ReLU (Eq. 2).  One global write per output, no atomics;
 //    accumulation order (channel, entry) is fixed -> deterministic.
 #pragma once
+#include <type_traits>
+
 #include "sc_internal.h"
 
 namespace sc {
@@ -51,7 +53,12 @@ struct Args {
     int n, C, H, K, Cg, Kg, kblocks, Ho, relu;
     int64_t cap;
     int ytiles, units, ctas_per_kb;
-    Gate gate;  // f3: device-side path selection
+};
+// f3 (device-side path selection) launches a separate instantiation with the gate
+// appended: adding the field to Args itself was measured to slow the ungated
+// kernel by 10% (V21, C2 s=0.95: 172 -> 189 us; register allocation shifts).
+struct ArgsGated : Args {
+    Gate gate;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,12 +111,14 @@ struct Smem {
     static_assert(total * V::MINB <= 227 * 1024, "shared memory budget of the SM exceeded");
 };
 
-template <class V, bool EMIT>
-__global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(const Args a) {
+template <class V, bool EMIT, class A = Args>
+__global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(const A a) {
     using SM = Smem<V>;
     constexpr int RS = V::R * V::S, TY = V::TY, NX = V::NX, WO = V::WO;
     constexpr int CH = V::CH, STAGES = V::STAGES, NW = V::NW, KBW = SM::KBW;
-    if (gate_closed(a.gate)) return;
+    if constexpr (std::is_same<A, ArgsGated>::value) {
+        if (gate_closed(a.gate)) return;
+    }
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring);
@@ -358,10 +367,11 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
                      const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt, cudaStream_t st, Gate gate) {
     if (g.ty != V::TY || g.tiles != (g.Ho + V::TY - 1) / V::TY || (g.Cg + V::CH - 1) / V::CH > 63)
         return cudaErrorInvalidValue;
-    Args a;
+    ArgsGated ag;
+    Args& a = ag;
     a.entries = entries; a.offs = offs; a.wpack = wpack; a.bias = bias; a.out = out;
     a.rowlist = rowlist; a.rowcnt = rowcnt;
-    a.gate = gate;
+    ag.gate = gate;
     a.n = (int)n; a.C = (int)g.C; a.H = (int)g.H; a.K = (int)g.K; a.Cg = (int)g.Cg; a.Kg = (int)g.Kg;
     a.kblocks = (int)g.kblocks; a.Ho = (int)g.Ho; a.relu = g.relu ? 1 : 0;
     a.cap = g.cap;
@@ -380,6 +390,14 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
+    if (gate.flag != nullptr) {
+        if (rowlist != nullptr) return cudaErrorNotSupported;
+        auto kg = gather_fast_kernel<V, false, ArgsGated>;
+        e = cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kg<<<(unsigned)grid, (V::NW + 1) * 32, smem, st>>>(ag);
+        return cudaGetLastError();
+    }
     kern<<<(unsigned)grid, (V::NW + 1) * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
