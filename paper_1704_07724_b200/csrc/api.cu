@@ -40,6 +40,11 @@ struct sc_plan_s {
     // f3 crossover: device words (nnz, ticket, path flag, last nnz) and s* (< 0: unset)
     unsigned long long* sel = nullptr;
     double s_star = -1.0;
+    // sparse_conv_forward_host pipeline (created on first use): copy-in, compute and
+    // copy-out streams, per-chunk events
+    static constexpr int kHostChunks = 8;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_in[kHostChunks] = {}, ev_comp[kHostChunks] = {}, ev_start = nullptr, ev_done = nullptr;
 };
 
 namespace {
@@ -167,6 +172,14 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
     cudaFree(p->sel);
+    for (auto& h : p->hs)
+        if (h) cudaStreamDestroy(h);
+    for (int i = 0; i < sc_plan_s::kHostChunks; ++i) {
+        if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
+        if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
+    }
+    if (p->ev_start) cudaEventDestroy(p->ev_start);
+    if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->bws);
     delete p;
 }
@@ -194,6 +207,19 @@ cudaError_t ensure_staging(sc_plan_s* p) {
     if (!p->stage_out && (e = cudaMalloc(&p->stage_out, sizeof(float) * g.N * g.K * g.Ho * g.Wo)) != cudaSuccess)
         return e;
     return cudaSuccess;
+}
+
+cudaError_t ensure_host_pipeline(sc_plan_s* p) {
+    cudaError_t e = cudaSuccess;
+    for (auto& h : p->hs)
+        if (!h && (e = cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    auto mk = [](cudaEvent_t* ev) {
+        return *ev ? cudaSuccess : cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    };
+    for (int i = 0; i < sc_plan_s::kHostChunks; ++i)
+        if ((e = mk(&p->ev_in[i])) != cudaSuccess || (e = mk(&p->ev_comp[i])) != cudaSuccess) return e;
+    if ((e = mk(&p->ev_start)) != cudaSuccess) return e;
+    return mk(&p->ev_done);
 }
 
 // Best-of-3 device time (us) of one path on the staged input (one untimed run first).
@@ -400,14 +426,48 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
     DeviceGuard guard(plan->device);
     const Geometry& g = plan->g;
     cudaError_t e;
-    if ((e = ensure_staging(plan)) != cudaSuccess) return cuda_fail(e, "staging alloc");
+    if ((e = ensure_staging(plan)) != cudaSuccess || (e = ensure_host_pipeline(plan)) != cudaSuccess)
+        return cuda_fail(e, "host pipeline setup");
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t nin = sizeof(float) * n * g.C * g.H * g.W, nout = sizeof(float) * n * g.K * g.Ho * g.Wo;
-    if ((e = cudaMemcpyAsync(plan->stage_in, h_in, nin, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return cuda_fail(e, "H2D copy");
-    if ((st = sparse_conv_forward(plan, n, plan->stage_in, plan->stage_out, stream)) != SC_OK) return st;
-    if ((e = cudaMemcpyAsync(h_out, plan->stage_out, nout, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-        return cuda_fail(e, "D2H copy");
+    cudaStream_t h2d = plan->hs[0], comp = plan->hs[1], d2h = plan->hs[2];
+    const int64_t in_img = g.C * g.H * g.W, out_img = g.K * g.Ho * g.Wo;
+    // chunks of whole images, boundaries at multiples of 4 images (16-byte aligned device
+    // pointers for any shape); chunk i's copy-in overlaps chunk i-1's kernels and chunk i-2's
+    // copy-out (separate copy engines for the two directions)
+    static const int max_chunks = [] {
+        const char* v = getenv("SC_HOST_CHUNKS");  // measurement knob, 1..kHostChunks
+        const int c = v ? atoi(v) : 4;
+        return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
+    }();
+    int chunks = (int)(n / 4 < max_chunks ? n / 4 : max_chunks);
+    if (chunks < 1) chunks = 1;
+    if ((e = cudaEventRecord(plan->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    for (cudaStream_t x : {h2d, comp, d2h})
+        if ((e = cudaStreamWaitEvent(x, plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    for (int i = 0; i < chunks; ++i) {
+        const int64_t c0 = i == 0 ? 0 : ((n * i / chunks) & ~(int64_t)3);
+        const int64_t c1 = i + 1 == chunks ? n : ((n * (i + 1) / chunks) & ~(int64_t)3);
+        if (c1 <= c0) continue;
+        const size_t bi = sizeof(float) * (c1 - c0) * in_img, bo = sizeof(float) * (c1 - c0) * out_img;
+        float* din = plan->stage_in + c0 * in_img;
+        float* dout = plan->stage_out + c0 * out_img;
+        if ((e = cudaMemcpyAsync(din, h_in + c0 * in_img, bi, cudaMemcpyHostToDevice, h2d)) != cudaSuccess ||
+            (e = cudaEventRecord(plan->ev_in[i], h2d)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(comp, plan->ev_in[i], 0)) != cudaSuccess)
+            return cuda_fail(e, "H2D copy");
+        // kernels run in chunk order on one stream: the plan's workspace is reused chunk to chunk
+        if ((e = enqueue_sparse(plan, c1 - c0, din, dout, comp)) != cudaSuccess) return cuda_fail(e, "forward");
+        if ((e = cudaEventRecord(plan->ev_comp[i], comp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(d2h, plan->ev_comp[i], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(h_out + c0 * out_img, dout, bo, cudaMemcpyDeviceToHost, d2h)) != cudaSuccess)
+            return cuda_fail(e, "D2H copy");
+    }
+    // the caller's stream resumes after everything (kernels and copies) of this call
+    if ((e = cudaEventRecord(plan->ev_done, d2h)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, plan->ev_done, 0)) != cudaSuccess ||
+        (e = cudaEventRecord(plan->ev_comp[0], comp)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, plan->ev_comp[0], 0)) != cudaSuccess)
+        return cuda_fail(e, "stream join");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
     return SC_OK;
 }

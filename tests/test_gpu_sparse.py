@@ -226,6 +226,25 @@ def test_forward_host_matches_device(sc):
     assert torch.equal(dev, h_out)
 
 
+@pytest.mark.parametrize("n,pinned", [(37, True), (16, False), (128, True)])
+def test_forward_host_pipelined_chunks(sc, n, pinned):
+    """The host path cuts the batch into up to 4 chunks (boundaries at multiples of
+    4 images, ragged last chunk) on its own streams: identical to the device path."""
+    shp = datagen.C2.with_batch(n)
+    x = datagen.activations(shp, 0.95, seed=17)
+    w, b = datagen.weights(shp, seed=17)
+    conv = make_conv(sc, shp, w, b, max_batch=128)
+    dev = conv.forward(torch.from_numpy(x).to(DEV)).cpu()
+    h_in = torch.from_numpy(x)
+    h_out = torch.full((n,) + conv.out_shape, float("nan"))
+    if pinned:
+        h_in, h_out = h_in.pin_memory(), h_out.pin_memory()
+    conv.forward_host(h_in, h_out)
+    assert torch.equal(dev, h_out)
+    conv.forward_host(h_in, h_out)  # repeated calls reuse the plan's streams and events
+    assert torch.equal(dev, h_out)
+
+
 def test_argument_errors(sc):
     shp = datagen.C4B.with_batch(2)
     w, b = datagen.weights(shp)
