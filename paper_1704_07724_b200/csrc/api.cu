@@ -439,14 +439,30 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
         const int c = v ? atoi(v) : 4;
         return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
     }();
+    static const int64_t first_env = [] {
+        const char* v = getenv("SC_HOST_FIRST");  // measurement knob: images in the first chunk (0: even split)
+        return (int64_t)(v ? atoi(v) : -1);
+    }();
     int chunks = (int)(n / 4 < max_chunks ? n / 4 : max_chunks);
     if (chunks < 1) chunks = 1;
+    // chunk boundaries (multiples of 4 images): a small first chunk starts the copy-out early
+    // (the copy-out of the dense fp32 output is the longest leg), the rest split evenly
+    int64_t bounds[sc_plan_s::kHostChunks + 1];
+    bounds[0] = 0;
+    int64_t first = first_env >= 0 ? first_env : n / 8;
+    first = (first + 3) & ~(int64_t)3;
+    if (chunks == 1 || first <= 0 || first >= n) {
+        for (int i = 1; i <= chunks; ++i) bounds[i] = i == chunks ? n : ((n * i / chunks) & ~(int64_t)3);
+    } else {
+        bounds[1] = first;
+        for (int i = 2; i <= chunks; ++i)
+            bounds[i] = i == chunks ? n : ((first + (n - first) * (i - 1) / (chunks - 1)) & ~(int64_t)3);
+    }
     if ((e = cudaEventRecord(plan->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
     for (cudaStream_t x : {h2d, comp, d2h})
         if ((e = cudaStreamWaitEvent(x, plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     for (int i = 0; i < chunks; ++i) {
-        const int64_t c0 = i == 0 ? 0 : ((n * i / chunks) & ~(int64_t)3);
-        const int64_t c1 = i + 1 == chunks ? n : ((n * (i + 1) / chunks) & ~(int64_t)3);
+        const int64_t c0 = bounds[i], c1 = bounds[i + 1];
         if (c1 <= c0) continue;
         const size_t bi = sizeof(float) * (c1 - c0) * in_img, bo = sizeof(float) * (c1 - c0) * out_img;
         float* din = plan->stage_in + c0 * in_img;
