@@ -10,8 +10,9 @@
 //
 // Two kernels per forward:
 //  1. nchw_to_nhwc: the input is transposed to channels-last and rounded to
-//     TF32 (cvt.rna) into a plan-owned buffer [N][H][W][Cp] (Cp = C rounded up
-//     to 4: 16-byte TMA strides), so that every (tap, 32-channel block) of a
+//     TF32 (cvt.rna) into a plan-owned buffer [N][H][W][Cp] (Cp = G * Cgp, each
+//     group's Cg channels padded to Cgp = a multiple of 4: 16-byte TMA strides and
+//     16-byte aligned box starts in the channel dimension), so that every (tap, 32-channel block) of a
 //     pixel tile is ONE 4-D TMA box: 32 channels x Wo columns x ROWS rows of one
 //     image, stride T in both spatial dimensions, zero-filled outside the image
 //     (that is the padding).  Each pixel row is 128 bytes = one SWIZZLE_128B
@@ -42,7 +43,7 @@ struct Args {
     const float* bias;
     float* out;
     int K, Kg, Cg, R, S, T, P, Ho, Wo, HoWo, relu;
-    int rows, ptiles, mtiles, cb, kblocks, npix, nmma;
+    int rows, ptiles, mtiles, cb, kblocks, npix, nmma, cgp;
     uint32_t idesc;
     Gate gate;
 };
@@ -92,9 +93,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
            ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
 
-// in [N][C][H*W] -> nhwc [N][H*W][Cp], TF32-rounded (RNA); channels >= C are 0.
+// in [N][C][H*W] -> nhwc [N][H*W][Cp], TF32-rounded (RNA), Cp = G*Cgp: group g's channel cl
+// (< Cg) at g*Cgp + cl, the padding channels cl in [Cg, Cgp) are 0.  Cgp = Cg rounded up to 4
+// keeps every group's first channel 16-byte aligned (a TMA box start in the channel
+// dimension must be a multiple of 16 bytes).
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                          int C, int Cp, int HW, Gate gate) {
+                                                          int C, int Cp, int Cg, int Cgp, int HW, Gate gate) {
     if (gate_closed(gate)) return;
     __shared__ float tile[32][33];
     const int n = blockIdx.z;
@@ -103,8 +107,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
     const float* src = in + (size_t)n * C * HW;
 #pragma unroll
     for (int i = 0; i < 32; i += 8) {
-        const int c = c0 + ty + i, p = p0 + tx;
-        tile[ty + i][tx] = (c < C && p < HW) ? to_tf32(__ldg(src + (size_t)c * HW + p)) : 0.f;
+        const int oc = c0 + ty + i, p = p0 + tx;  // output channel oc = g*Cgp + cl
+        const int g = oc / Cgp, cl = oc - g * Cgp;
+        tile[ty + i][tx] = (oc < Cp && cl < Cg && p < HW) ? to_tf32(__ldg(src + (size_t)(g * Cg + cl) * HW + p)) : 0.f;
     }
     __syncthreads();
     float* dst = out + (size_t)n * HW * Cp;
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                 const int r = rs / a.S, t = rs - r * a.S;
                 mbar_expect_tx(&full[s], kATileBytes + bbytes);
                 tma_bulk_g2s(sA + s * kATileBytes, asrc + (size_t)kb * (kATileBytes / 4), kATileBytes, &full[s]);
-                tma_load_4d(sB + s * kBTileBytes, &bmap, g * a.Cg + cb * BK, t - a.P, y0 * a.T + r - a.P, n, &full[s]);
+                tma_load_4d(sB + s * kBTileBytes, &bmap, g * a.cgp + cb * BK, t - a.P, y0 * a.T + r - a.P, n, &full[s]);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -298,7 +303,8 @@ EncodeTiled encoder() {
 // pixel tile of whole output rows cannot fit one UMMA N <= 256 or a TMA box.
 void dense_geometry(const Geometry& g, DenseGeom* dg) {
     using namespace dense;
-    dg->cp = (g.C + 3) / 4 * 4;
+    dg->cgp = (g.Cg + 3) / 4 * 4;
+    dg->cp = g.G * dg->cgp;
     dg->cb = (g.Cg + BK - 1) / BK;
     dg->kblocks = g.R * g.S * dg->cb;
     dg->mtiles = (g.Kg + BM - 1) / BM;
@@ -345,7 +351,7 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     if (!dg.supported) return cudaErrorNotSupported;
     const int HW = (int)(g.H * g.W);
     dim3 tgrid((unsigned)((HW + 31) / 32), (unsigned)((dg.cp + 31) / 32), (unsigned)n);
-    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, HW, gate);
+    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, (int)g.Cg, (int)dg.cgp, HW, gate);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     Args a;
@@ -357,7 +363,7 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     a.relu = g.relu ? 1 : 0;
     a.gate = gate;
     a.rows = (int)dg.rows; a.ptiles = (int)dg.ptiles; a.mtiles = (int)dg.mtiles; a.cb = (int)dg.cb;
-    a.kblocks = (int)dg.kblocks; a.npix = (int)dg.npix; a.nmma = (int)dg.nmma;
+    a.kblocks = (int)dg.kblocks; a.npix = (int)dg.npix; a.nmma = (int)dg.nmma; a.cgp = (int)dg.cgp;
     // instruction descriptor: D f32 [4,6)=1, A tf32 [7,10)=2, B tf32 [10,13)=2, both K-major,
     // N>>3 at [17,23), M>>4 at [24,29)
     a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(dg.nmma >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);

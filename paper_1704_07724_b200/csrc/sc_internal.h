@@ -32,11 +32,11 @@ struct Geometry {
     bool relu;
 };
 
-// Dense tcgen05 path geometry (dense_tc.cu): channels-last input with Cp = C
-// rounded up to 4; K-dim blocks of 32 channels per tap (cb per group); tiles
+// Dense tcgen05 path geometry (dense_tc.cu): channels-last input with Cp = G*Cgp
+// channels (each group's Cg padded to a multiple of 4); K-dim blocks of 32 channels per tap (cb per group); tiles
 // of `rows` whole output rows (npix = rows*Wo pixels, UMMA N = nmma).
 struct DenseGeom {
-    int64_t cp, cb, kblocks, mtiles, rows, ptiles, npix, nmma;
+    int64_t cp, cgp, cb, kblocks, mtiles, rows, ptiles, npix, nmma;  // cp = G * cgp, cgp = Cg rounded up to 4
     bool supported;
 };
 

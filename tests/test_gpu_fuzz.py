@@ -1,0 +1,113 @@
+"""Seeded shape fuzz through the C ABI: shapes away from the BASELINE configs,
+so that every fallback is exercised — the generic stage-2 kernel (widths with
+no generated variant), the streamwise stage 1 (planes > 1024 elements or > 31
+rows), strides 1-3, pads 0-3, groups 1-4, rectangular kernels, filter counts
+that are not multiples of 32, one-pixel planes and outputs.
+
+Per shape: stage-1 streams bit-exact against oracle.compact_streams; sparse
+forward within the north-star bar 1e-5*mass + 1e-6; dense forward (where the
+shape is supported) within the TF32 bar 2^-9*mass + 1e-6; integer data
+bit-exact on both; backward (where supported) bit-exact on integer data."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1704_07724_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def sc():
+    from paper_1704_07724_b200 import sparseconv
+    sparseconv.lib()
+    return sparseconv
+
+
+def fuzz_shapes(count=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    fixed = [  # hand-picked corners
+        datagen.ConvShape("one_pixel", 900, 2, 3, 1, 1, 5, 1, 1, 1, 0, 1),          # 1x1 plane, 1x1 kernel
+        datagen.ConvShape("kernel_eq_plane", 901, 2, 4, 5, 5, 7, 5, 5, 1, 0, 1),    # one output pixel
+        datagen.ConvShape("big_pad", 902, 2, 3, 4, 4, 6, 3, 3, 1, 3, 1),            # pad > kernel/2
+        datagen.ConvShape("large_plane", 903, 2, 6, 40, 36, 33, 3, 3, 1, 1, 1),     # streamwise stage 1
+        datagen.ConvShape("tall_plane", 904, 2, 5, 48, 9, 17, 3, 3, 2, 1, 1),       # > 31 rows, stride 2
+        datagen.ConvShape("rect_kernel", 905, 3, 8, 10, 12, 40, 3, 5, 1, 2, 2),     # R != S, groups 2
+        datagen.ConvShape("stride3", 906, 2, 6, 17, 17, 20, 5, 5, 3, 2, 1),
+        datagen.ConvShape("groups4", 907, 2, 16, 9, 9, 36, 3, 3, 1, 1, 4),
+    ]
+    out = list(fixed)
+    for i in range(count - len(fixed)):
+        groups = int(rng.choice([1, 1, 2, 3]))
+        c = groups * int(rng.integers(1, 9))
+        k = groups * int(rng.integers(1, 25))
+        h, w = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+        stride = int(rng.choice([1, 1, 2, 3]))
+        pad = int(rng.integers(0, 4))
+        r = int(rng.integers(1, min(7, h + 2 * pad) + 1))
+        s = int(rng.integers(1, min(7, w + 2 * pad) + 1))
+        n = int(rng.integers(1, 5))
+        out.append(datagen.ConvShape(f"rand{seed}_{i}", 910 + i, n, c, h, w, k, r, s, stride, pad, groups))
+    return out
+
+
+SHAPES = fuzz_shapes() + fuzz_shapes(count=32, seed=77)[8:]
+
+
+def make_conv(sc, shp, w, b):
+    return sc.SparseConv(torch.from_numpy(w).to(DEV), None if b is None else torch.from_numpy(b).to(DEV), shp.n,
+                         shp.c, shp.h, shp.w, shp.stride, shp.pad, shp.groups)
+
+
+@pytest.mark.parametrize("shp", SHAPES, ids=[s.name for s in SHAPES])
+def test_fuzz_shape(sc, shp):
+    x = datagen.activations(shp, 0.7, seed=5)
+    w, b = datagen.weights(shp, seed=5)
+    conv = make_conv(sc, shp, w, b)
+    xd = torch.from_numpy(x).to(DEV)
+    out = conv.forward(xd).cpu().numpy()
+    # stage 1 bit-exact
+    lists = conv.lists(shp.n)
+    ref_l = oracle.compact_streams(x, shp.r, shp.stride, shp.pad, lists["ty"])
+    offs = lists["offs"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(offs, ref_l["offs"])
+    length = ref_l["offs"][:, :, -1]
+    valid = np.arange(ref_l["cap"])[None, None, :] < length[:, :, None]
+    ge = lists["entries"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref_l["entries"], 0))
+    # forward, sparse and dense
+    ref, mass = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
+    assert np.all(np.abs(out - ref) <= oracle.tolerance_sparse(mass)), conv.variant
+    try:
+        dense = conv.dense_forward(xd).cpu().numpy()
+    except sc.SparseConvError:
+        dense = None
+    if dense is not None:
+        assert np.all(np.abs(dense - ref) <= oracle.tolerance_dense_tf32(mass))
+    # integer data: exact on every path
+    xi, wi, bi = datagen.integer_case(shp, sparsity=0.6, seed=5)
+    convi = make_conv(sc, shp, wi, bi)
+    xid = torch.from_numpy(xi).to(DEV)
+    refi, _ = oracle.conv_fp64(xi, wi, bi, shp.stride, shp.pad, shp.groups, want_mass=False)
+    assert np.array_equal(convi.forward(xid).cpu().numpy().astype(np.float64), refi)
+    if dense is not None:
+        assert np.array_equal(convi.dense_forward(xid).cpu().numpy().astype(np.float64), refi)
+    di = np.random.default_rng(5).integers(-3, 4, (shp.n, shp.k, shp.ho, shp.wo)).astype(np.float32)
+    try:
+        dw, db, dz = convi.backward(xid, torch.from_numpy(di).to(DEV))
+    except sc.SparseConvError:
+        return  # backward: plane-major shapes with 1x1 / 3x3 / 5x5 kernels only (documented)
+    refb = oracle.conv_backward_fp64(xi, wi, di, shp.stride, shp.pad, shp.groups, want_mass=False)
+    assert np.array_equal(dw.cpu().numpy().astype(np.float64), refb["dw"])
+    assert np.array_equal(db.cpu().numpy().astype(np.float64), refb["dbias"])
+    assert np.array_equal(dz.cpu().numpy().astype(np.float64), refb["dz"])
+
+
+def test_too_large_is_unsupported(sc):
+    """Element counts >= 2^31 are rejected before any allocation."""
+    w = torch.zeros((8, 64, 3, 3), device=DEV)
+    with pytest.raises(sc.SparseConvError) as e:
+        sc.SparseConv(w, None, 2048, 64, 128, 128, pad=1)  # input 2048*64*128*128 = 2^31 elements
+    assert e.value.status == 3  # SC_ERR_UNSUPPORTED
