@@ -111,3 +111,71 @@ def test_too_large_is_unsupported(sc):
     with pytest.raises(sc.SparseConvError) as e:
         sc.SparseConv(w, None, 2048, 64, 128, 128, pad=1)  # input 2048*64*128*128 = 2^31 elements
     assert e.value.status == 3  # SC_ERR_UNSUPPORTED
+
+
+def chain_shapes():
+    """Random 3-layer chains (layer l+1's input = layer l's output), ReLU fused between layers."""
+    rng = np.random.default_rng(4242)
+    chains = []
+    for ci in range(6):
+        n = int(rng.integers(1, 4))
+        c, h, w = int(rng.integers(1, 40)), int(rng.integers(3, 16)), int(rng.integers(3, 30))
+        layers = []
+        fast = ci < 3  # widths with generated 3x3 kernels (V21 13, V44 14, V46 7): fused emission
+        if fast:
+            h = w = int([13, 14, 7][ci])
+        for li in range(3):
+            r = 3 if fast else int(rng.choice([1, 3, 5]))
+            pad = 1 if fast else (r // 2 if rng.random() < 0.8 else 0)
+            if r > h + 2 * pad or r > w + 2 * pad:
+                r, pad = 1, 0
+            k = int(rng.integers(1, 70))
+            shp = datagen.ConvShape(f"chain{ci}_l{li}", 960 + 3 * ci + li, n, c, h, w, k, r, r, 1, pad, 1)
+            layers.append(shp)
+            c, h, w = k, shp.ho, shp.wo
+        chains.append(layers)
+    return chains
+
+
+@pytest.mark.parametrize("ci", range(6))
+@pytest.mark.parametrize("fused", [False, True])
+def test_fuzz_chain(sc, ci, fused):
+    """sparse_conv_forward_chain on random 3-layer chains, with materialised or (where the layer's
+    kernel can emit lists) fused intermediates: the last output equals running the layers one by
+    one through sparse_conv_forward, and every layer matches the oracle on its GPU input (R14)."""
+    layers = chain_shapes()[ci]
+    n = layers[0].n
+    convs, ws = [], []
+    for li, shp in enumerate(layers):
+        w, b = datagen.weights(shp, seed=3, std=0.3)
+        ws.append((w, b))
+        convs.append(make_conv_relu(sc, shp, w, b, relu=li + 1 < len(layers)))
+    x = torch.from_numpy(datagen.activations(layers[0], 0.8, seed=3)).to(DEV)
+    outs = [torch.empty((n,) + c.out_shape, device=DEV) for c in convs]
+    if fused:
+        for li in range(len(convs) - 1):
+            vid, name = convs[li].variant
+            if vid > 0 and "_kl1" not in name:  # KL >= 2 fast kernels emit the next layer's lists
+                outs[li] = None
+    if fused and ci < 3:
+        assert outs[0] is None and outs[1] is None, [c.variant for c in convs]
+    sc.chain_forward(convs, x, outs)
+    # layer by layer reference through the single-layer entry point
+    cur = x
+    for li, (conv, shp) in enumerate(zip(convs, layers)):
+        y = conv.forward(cur)
+        torch.cuda.synchronize()
+        w, b = ws[li]
+        ref, mass = oracle.conv_fp64(cur.cpu().numpy(), w, b, shp.stride, shp.pad, shp.groups)
+        if li + 1 < len(layers):
+            ref = np.maximum(ref, 0.0)
+        assert np.all(np.abs(y.cpu().numpy() - ref) <= oracle.tolerance_sparse(mass)), f"layer {li}"
+        if outs[li] is not None:
+            assert torch.equal(outs[li], y), f"chain layer {li} differs from the single-layer forward"
+        cur = y
+    assert torch.equal(outs[-1], cur)
+
+
+def make_conv_relu(sc, shp, w, b, relu):
+    return sc.SparseConv(torch.from_numpy(w).to(DEV), torch.from_numpy(b).to(DEV), shp.n, shp.c, shp.h, shp.w,
+                         shp.stride, shp.pad, shp.groups, fuse_relu=relu)
