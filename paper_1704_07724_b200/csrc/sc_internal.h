@@ -5,19 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sc_device.h"
 #include "sparse_conv.h"
 
 namespace sc {
-
-// Device-side path selection: a kernel launched with a gate
-// returns at once unless *flag == run_if (flag null: always runs).  Lets the
-// sparse and the dense path both be enqueued (graph-capturable) while only the
-// one chosen on the device from the batch's measured density does work.
-struct Gate {
-    const int* flag = nullptr;
-    int run_if = 0;
-};
-__device__ __forceinline__ bool gate_closed(const Gate& g) { return g.flag != nullptr && *g.flag != g.run_if; }
 
 // Geometry derived once at plan creation.
 struct Geometry {
