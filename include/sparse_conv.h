@@ -246,6 +246,16 @@ sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t *variant, const char 
  * supported, else 1 + sparse). */
 sc_status sparse_conv_launch_count(sc_plan plan, int32_t *sparse_launches, int32_t *dense_launches);
 
+/* Source of a stage-2 interpreter variant as generated at run time for shapes
+ * without a shipped variant (csrc/jit.cu, compiled through NVRTC when a plan is
+ * created); tests compare it with tools/gen_gather.py.  params = {R, S, P, T, W,
+ * TY, KL, NW, MINB, CH, STAGES, SLOTS, PIECE, id}.  Writes at most cap-1 bytes
+ * plus a NUL into buf (may be NULL) and returns the full length.  Host only. */
+size_t sc_jit_variant_source(const int32_t params[14], char *buf, size_t cap);
+/* 1 if run-time variant generation is available (NVRTC and the driver entry
+ * points load), else 0; plans then use the generic stage-2 kernel instead. */
+int32_t sc_jit_available(void);
+
 /* Micro-probes for the roofline denominators (bench only).  Each runs on the
  * current device and stream 0 and synchronizes.
  *   kind 0: FFMA  (3-register form) lanes-FMA per SM-clock

@@ -32,8 +32,13 @@ struct sc_plan_s {
     uint32_t* cnt = nullptr;   // stage-1 counts [N][tiles][C] (plane-major compaction)
     uint2* plist = nullptr;    // stage-1 per-plane compacted lists [N*C][H*W]
     uint32_t* prow = nullptr;  // stage-1 per-plane row prefixes [N*C][H+1]
-    int variant = 0;
+    int variant = 0;           // > 0 generated variant, 0 generic kernel, -1 run-time generated (jit.cu)
     const char* variant_name = "generic";
+    sc::jit::Params jp;        // variant -1: its parameters, kernels (ungated, gated) and shared memory
+    void* jit_fn = nullptr;
+    void* jit_fn_gated = nullptr;
+    size_t jit_smem = 0;
+    char jit_name[96] = {0};
     // staging for sparse_conv_forward_host and calibration (allocated on first use)
     float* stage_in = nullptr;
     float* stage_out = nullptr;
@@ -94,21 +99,31 @@ void stream_format(Geometry* g, int64_t ty) {
     g->cap += g->cap & 1;  // even: every stream starts 16-byte aligned
 }
 
-// Choose the stage-2 kernel (SC_FORCE_VARIANT env: -1 auto, 0 generic, id) and
-// fix what it implies: packed-weight k-block width and the stream row tiles.
-void choose_kernel(Geometry* g, int* variant, const char** name) {
+// Choose the stage-2 kernel (SC_FORCE_VARIANT env: -1 auto, 0 generic, id; SC_NO_JIT
+// env: never generate at run time) and fix what it implies: packed-weight k-block
+// width and the stream row tiles.  No generated variant matches -> a run-time
+// generated one (variant -1, parameters in *jp) if allow_jit and the shape is in range.
+void choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit, sc::jit::Params* jp) {
     int force = -1;
     if (const char* f = getenv("SC_FORCE_VARIANT")) force = atoi(f);
     int kl = 1, ty = (int)g->Ho;
     *variant = sc::gather_fast_select(*g, force, name, &kl, &ty);
     if (*variant == 0) *name = "generic";
+    if (*variant == 0 && allow_jit && force != 0 && !getenv("SC_NO_JIT") && sc::jit::available() &&
+        sc::jit::choose(*g, jp)) {
+        *variant = -1;
+        *name = "jit";
+        kl = jp->KL;
+        ty = jp->TY;
+    }
     g->kbw = 32 * kl;
     g->Kg_pad = (g->Kg + g->kbw - 1) / g->kbw * g->kbw;
     g->kblocks = g->Kg_pad / g->kbw;
     stream_format(g, ty);
 }
 
-sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int* variant, const char** name) {
+sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int* variant, const char** name,
+                        bool allow_jit = false, sc::jit::Params* jp = nullptr) {
     g->N = p->n; g->C = p->c; g->H = p->h; g->W = p->w; g->K = p->k; g->R = p->r; g->S = p->s;
     g->T = p->stride; g->P = p->pad; g->G = p->groups;
     g->Ho = (p->h + 2 * p->pad - p->r) / p->stride + 1;
@@ -116,7 +131,8 @@ sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int
     g->Cg = p->c / p->groups;
     g->Kg = p->k / p->groups;
     g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
-    choose_kernel(g, variant, name);
+    sc::jit::Params unused;
+    choose_kernel(g, variant, name, allow_jit && jp, jp ? jp : &unused);
     sc::dense_geometry(*g, dg);
     const int64_t in_e = g->N * g->C * g->H * g->W, out_e = g->N * g->K * g->Ho * g->Wo;
     const int64_t w_e = g->G * g->Cg * g->R * g->S * g->Kg_pad;
@@ -184,15 +200,25 @@ void free_plan(sc_plan_s* p) {
     delete p;
 }
 
+// Stage 2 with the plan's kernel (generated, run-time generated or generic).
+cudaError_t launch_stage2(sc_plan_s* p, int64_t n, const uint2* entries, const uint32_t* offs, float* out,
+                          uint2* rowlist, uint32_t* rowcnt, cudaStream_t s, sc::Gate gate = {}) {
+    if (p->variant > 0)
+        return sc::launch_gather_fast(p->variant, p->g, n, entries, offs, p->wpack, p->bias, out, rowlist, rowcnt, s,
+                                      gate);
+    if (rowlist) return cudaErrorNotSupported;
+    if (p->variant < 0)
+        return sc::jit::launch(gate.flag ? p->jit_fn_gated : p->jit_fn, p->jit_smem, p->jp, p->g, n, entries, offs,
+                               p->wpack, p->bias, out, s, gate);
+    return sc::launch_gather_generic(p->g, n, entries, offs, p->wpack, p->bias, out, s, gate);
+}
+
 // stage 1 + stage 2 of the sparse path (gated: f3)
 cudaError_t enqueue_sparse(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
                            sc::Gate gate = {}) {
     cudaError_t e = sc::launch_compact(p->g, n, d_in, p->cnt, p->plist, p->prow, p->entries, p->offs, s, gate);
     if (e != cudaSuccess) return e;
-    if (p->variant > 0)
-        return sc::launch_gather_fast(p->variant, p->g, n, p->entries, p->offs, p->wpack, p->bias, d_out, nullptr,
-                                      nullptr, s, gate);
-    return sc::launch_gather_generic(p->g, n, p->entries, p->offs, p->wpack, p->bias, d_out, s, gate);
+    return launch_stage2(p, n, p->entries, p->offs, d_out, nullptr, nullptr, s, gate);
 }
 
 cudaError_t enqueue_dense(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
@@ -316,11 +342,23 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
     if (!plan) return fail(SC_ERR_OUT_OF_MEMORY, "host allocation failed");
     plan->params = *params;
     plan->device = device;
-    if ((st = make_geometry(params, &plan->g, &plan->dg, &plan->variant, &plan->variant_name)) != SC_OK) {
+    DeviceGuard guard(device);
+    if ((st = make_geometry(params, &plan->g, &plan->dg, &plan->variant, &plan->variant_name, true, &plan->jp)) !=
+        SC_OK) {
         delete plan;
         return st;
     }
-    DeviceGuard guard(device);
+    if (plan->variant < 0) {  // compile the run-time variant now; on failure keep the generic kernel
+        if (sc::jit::compile(plan->jp, device, &plan->jit_fn, &plan->jit_fn_gated, &plan->jit_smem) == cudaSuccess) {
+            const sc::jit::Params& q = plan->jp;
+            snprintf(plan->jit_name, sizeof(plan->jit_name), "jit_r%ds%dp%dt%d_w%d_ty%d_kl%d_nw%d_ch%d", q.R, q.S,
+                     q.P, q.T, q.W, q.TY, q.KL, q.NW, q.CH);
+            plan->variant_name = plan->jit_name;
+        } else if ((st = make_geometry(params, &plan->g, &plan->dg, &plan->variant, &plan->variant_name)) != SC_OK) {
+            delete plan;
+            return st;
+        }
+    }
     if ((st = check_dev_ptr(plan, d_weight, "d_weight")) != SC_OK ||
         (d_bias && (st = check_dev_ptr(plan, d_bias, "d_bias")) != SC_OK)) {
         delete plan;
@@ -393,12 +431,7 @@ sc_status sparse_conv_gather(sc_plan plan, int64_t n, float* d_out, sc_stream_t 
     if ((st = check_dev_ptr(plan, d_out, "d_out")) != SC_OK) return st;
     DeviceGuard guard(plan->device);
     cudaError_t e;
-    if (plan->variant > 0)
-        e = sc::launch_gather_fast(plan->variant, plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias,
-                                   d_out, nullptr, nullptr, (cudaStream_t)stream);
-    else
-        e = sc::launch_gather_generic(plan->g, n, plan->entries, plan->offs, plan->wpack, plan->bias, d_out,
-                                      (cudaStream_t)stream);
+    e = launch_stage2(plan, n, plan->entries, plan->offs, d_out, nullptr, nullptr, (cudaStream_t)stream);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "gather launch");
 }
 
@@ -530,11 +563,8 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
                           sc::compact_uses_counts(next->g) && next->plist && next->prow;
         float* out = d_outs[l];
         if (!emit && !out) return fail(SC_ERR_UNSUPPORTED, "layer %d needs an output buffer (no list emission)", l);
-        if (p->variant > 0)
-            e = sc::launch_gather_fast(p->variant, p->g, n, p->entries, p->offs, p->wpack, p->bias, out,
-                                       emit ? next->plist : nullptr, emit ? next->prow : nullptr, s);
-        else
-            e = sc::launch_gather_generic(p->g, n, p->entries, p->offs, p->wpack, p->bias, out, s);
+        e = launch_stage2(p, n, p->entries, p->offs, out, emit ? next->plist : nullptr, emit ? next->prow : nullptr,
+                          s);
         if (e != cudaSuccess) return cuda_fail(e, "chain gather");
         lists_ready = emit;
     }
@@ -698,6 +728,17 @@ sc_status sparse_conv_launch_count(sc_plan plan, int32_t* sparse_launches, int32
     if (dense_launches) *dense_launches = 2;
     return SC_OK;
 }
+
+size_t sc_jit_variant_source(const int32_t params[14], char* buf, size_t cap) {
+    if (!params) return 0;
+    sc::jit::Params q;
+    q.R = params[0]; q.S = params[1]; q.P = params[2]; q.T = params[3]; q.W = params[4]; q.TY = params[5];
+    q.KL = params[6]; q.NW = params[7]; q.MINB = params[8]; q.CH = params[9]; q.STAGES = params[10];
+    q.SLOTS = params[11]; q.PIECE = params[12]; q.id = params[13];
+    return sc::jit::variant_source(q, buf, cap);
+}
+
+int32_t sc_jit_available(void) { return sc::jit::available() ? 1 : 0; }
 
 sc_status sc_probe_fma(int32_t kind, double* fma_per_clk_per_sm) {
     if (!fma_per_clk_per_sm || kind < 0 || kind > 2) return fail(SC_ERR_INVALID_ARGUMENT, "bad probe arguments");

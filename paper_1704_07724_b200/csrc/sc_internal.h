@@ -97,6 +97,25 @@ cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, cons
                             const float* dout, const float* wpack, float* ws, float* dw, float* dbias, float* dz,
                             cudaStream_t st);
 
+// Run-time specialised stage 2 (jit.cu): a gather variant generated for the plan's
+// shape and compiled through NVRTC when no generated variant matches.
+namespace jit {
+struct Params {
+    int R = 0, S = 0, P = 0, T = 1, W = 0, TY = 1, KL = 1, NW = 11, MINB = 1, CH = 16, STAGES = 2, SLOTS = 3,
+        PIECE = 254, id = 1000;
+};
+bool available();                                 // NVRTC and the driver entry points are loadable
+bool choose(const Geometry& g, Params* p);       // false: shape outside the generator's limits
+// Compile (cached per parameter set and device) the ungated and the gated kernel.
+cudaError_t compile(const Params& p, int device, void** fn, void** fn_gated, size_t* smem);
+cudaError_t launch(void* fn, size_t smem, const Params& p, const Geometry& g, int64_t n, const uint2* entries,
+                   const uint32_t* offs, const float* wpack, const float* bias, float* out, cudaStream_t st,
+                   Gate gate = {});
+const char* last_log();
+// Generated source of a variant (tests: must equal tools/gen_gather.py's); returns its length.
+size_t variant_source(const Params& p, char* buf, size_t cap);
+}  // namespace jit
+
 cudaError_t probe_fma(int kind, double* rate);
 cudaError_t launch_flush(void* scratch, size_t bytes, cudaStream_t st);
 

@@ -24,7 +24,8 @@ EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forwar
            "sparse_conv_compact", "sparse_conv_gather", "sparse_conv_lists", "sparse_conv_kernel_variant",
            "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
            "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
-           "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward")
+           "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward", "sc_jit_variant_source",
+           "sc_jit_available")
 SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
@@ -78,9 +79,12 @@ def lib():
         L.sc_status_string.argtypes = [st]
         L.sc_status_string.restype = ctypes.c_char_p
         L.sc_last_error.restype = ctypes.c_char_p
+        L.sc_jit_variant_source.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_char_p, ctypes.c_size_t]
         for fn in EXPORTS:
-            if fn not in ("sc_status_string", "sc_last_error"):
+            if fn not in ("sc_status_string", "sc_last_error", "sc_jit_variant_source", "sc_jit_available"):
                 getattr(L, fn).restype = st
+        L.sc_jit_variant_source.restype = ctypes.c_size_t
+        L.sc_jit_available.restype = ctypes.c_int32
         _lib = L
     return _lib
 
@@ -297,6 +301,15 @@ def chain_forward(convs, x, outs, stream=None):
     _check(lib().sparse_conv_forward_chain(plans, len(convs), n, ctypes.c_void_p(x.data_ptr()), ptrs,
                                            _stream_handle(stream)))
     return outs[-1]
+
+
+def jit_variant_source(R, S, P, T, W, TY, KL, NW=11, MINB=1, CH=16, STAGES=2, SLOTS=3, PIECE=254, vid=1000):
+    """Source text of a stage-2 variant generated by the library at run time (test hook)."""
+    p = (ctypes.c_int32 * 14)(R, S, P, T, W, TY, KL, NW, MINB, CH, STAGES, SLOTS, PIECE, vid)
+    n = lib().sc_jit_variant_source(p, None, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib().sc_jit_variant_source(p, buf, n + 1)
+    return buf.value.decode()
 
 
 def probe_fma(kind):

@@ -179,3 +179,43 @@ def test_fuzz_chain(sc, ci, fused):
 def make_conv_relu(sc, shp, w, b, relu):
     return sc.SparseConv(torch.from_numpy(w).to(DEV), torch.from_numpy(b).to(DEV), shp.n, shp.c, shp.h, shp.w,
                          shp.stride, shp.pad, shp.groups, fuse_relu=relu)
+
+
+JIT_SHAPES = [  # no shipped variant: the plan generates one at creation (csrc/jit.cu)
+    datagen.ConvShape("jit_w56_kl2", 980, 2, 8, 6, 56, 64, 3, 3, 1, 1, 1),
+    datagen.ConvShape("jit_w20_kl4", 981, 2, 12, 20, 20, 130, 3, 3, 1, 1, 1),
+    datagen.ConvShape("jit_s2_w32", 982, 2, 8, 32, 32, 100, 3, 3, 2, 1, 1),
+    datagen.ConvShape("jit_1x1_w17", 983, 2, 40, 17, 17, 128, 1, 1, 1, 0, 1),
+    datagen.ConvShape("jit_xpair_w12", 984, 3, 8, 10, 12, 20, 3, 5, 1, 2, 2),
+    datagen.ConvShape("jit_kl3_w9", 985, 2, 16, 9, 9, 80, 5, 5, 1, 2, 1),
+]
+
+
+@pytest.mark.parametrize("shp", JIT_SHAPES, ids=[s.name for s in JIT_SHAPES])
+def test_jit_variant(sc, shp):
+    if not sc.lib().sc_jit_available():
+        pytest.skip("NVRTC not loadable")
+    x = datagen.activations(shp, 0.9, seed=8)
+    w, b = datagen.weights(shp, seed=8)
+    conv = make_conv(sc, shp, w, b)
+    vid, name = conv.variant
+    assert vid == -1 and name.startswith("jit_"), name
+    xd = torch.from_numpy(x).to(DEV)
+    out = conv.forward(xd).cpu().numpy()
+    ref, mass = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
+    assert np.all(np.abs(out - ref) <= oracle.tolerance_sparse(mass))
+    xi, wi, bi = datagen.integer_case(shp, sparsity=0.6, seed=8)
+    refi, _ = oracle.conv_fp64(xi, wi, bi, shp.stride, shp.pad, shp.groups, want_mass=False)
+    assert np.array_equal(make_conv(sc, shp, wi, bi).forward(torch.from_numpy(xi).to(DEV)).cpu().numpy(), refi)
+    # the gated instantiation (device-side crossover) on the same plan
+    for s_star, want in ((0.0, sc.SC_PATH_SPARSE), (1.0, sc.SC_PATH_DENSE)):
+        conv.crossover = s_star
+        try:
+            o = conv.forward_auto(xd).cpu().numpy()
+        except sc.SparseConvError:
+            continue
+        path, _ = conv.last_path()
+        if path == sc.SC_PATH_SPARSE:
+            assert np.all(np.abs(o - ref) <= oracle.tolerance_sparse(mass))
+        else:
+            assert np.all(np.abs(o - ref) <= oracle.tolerance_dense_tf32(mass))
