@@ -25,7 +25,7 @@ def sc():
 def declared_functions():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:sc_status|const char \*)\s*(\w+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(?:sc_status|const char \*|size_t|int32_t)\s*(\w+)\s*\(", txt)))
 
 
 def test_header_declares_the_boundary():
