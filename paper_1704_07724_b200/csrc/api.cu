@@ -109,6 +109,22 @@ void choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit,
     int kl = 1, ty = (int)g->Ho;
     *variant = sc::gather_fast_select(*g, force, name, &kl, &ty);
     if (*variant == 0) *name = "generic";
+    // tuning knob: SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE" generates that variant for any shape
+    if (const char* jf = getenv("SC_JIT_FORCE")) {
+        if (allow_jit && sc::jit::available()) {
+            sc::jit::Params q;
+            if (sscanf(jf, "%d,%d,%d,%d,%d,%d,%d,%d", &q.TY, &q.KL, &q.NW, &q.MINB, &q.CH, &q.STAGES, &q.SLOTS,
+                       &q.PIECE) == 8) {
+                q.R = (int)g->R; q.S = (int)g->S; q.P = (int)g->P; q.T = (int)g->T; q.W = (int)g->W;
+                *jp = q;
+                *variant = -1;
+                *name = "jit";
+                kl = q.KL;
+                ty = q.TY;
+                allow_jit = false;
+            }
+        }
+    }
     if (*variant == 0 && allow_jit && force != 0 && !getenv("SC_NO_JIT") && sc::jit::available() &&
         sc::jit::choose(*g, jp)) {
         *variant = -1;

@@ -1,0 +1,57 @@
+"""Sweep run-time generated stage-2 variants for one config (SC_JIT_FORCE knob):
+python tools/jit_tune.py C2 0.95 [quick]
+Prints one line per parameter set: gather time (graph, warm L2), max err/tol on two
+oracle images, sorted by time at the end."""
+import itertools
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_1704_07724_b200 import datagen, sparseconv as sc  # noqa: E402
+from tools.probe_run import dev_time_us  # noqa: E402
+
+cfg, s = sys.argv[1], float(sys.argv[2])
+quick = len(sys.argv) > 3
+shp = datagen.CONFIGS[cfg]
+w, b = datagen.weights(shp)
+xh = datagen.activations(shp, s)
+x = torch.from_numpy(xh).cuda()
+refs = {i: oracle.conv_fp64(xh[i:i + 1], w, b, shp.stride, shp.pad, shp.groups) for i in (0, shp.n - 1)}
+out = torch.empty((shp.n, shp.k, shp.ho, shp.wo), device="cuda")
+
+grid = [(2, 4), (1, 4), (2, 2), (3, 2), (4, 2), (2, 3), (3, 3)]
+if shp.k // shp.groups <= 64 and shp.stride == 1:  # few filters: x-pair tiles (KL=1) too
+    grid += [(2, 1), (4, 1), (7, 1), (1, 1)]
+nws = [11, 9] if not quick else [11]
+chs = [16, 32, 8] if not quick else [16]
+stages = [2, 3]
+slots = [3, 4, 2]
+pieces = [254, 510, 126]
+res = []
+for (ty, kl), nw, ch, st, sl, pc in itertools.product(grid, nws, chs, stages, slots, pieces):
+    os.environ["SC_JIT_FORCE"] = f"{ty},{kl},{nw},1,{ch},{st},{sl},{pc}"
+    try:
+        conv = sc.SparseConv(torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), shp.n, shp.c, shp.h, shp.w,
+                             shp.stride, shp.pad, shp.groups)
+    except sc.SparseConvError as e:
+        print(os.environ["SC_JIT_FORCE"], "create failed", e, flush=True)
+        continue
+    if conv.variant[0] != -1:
+        continue  # compile failed (e.g. shared memory) -> generic
+    conv.forward(x, out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    worst = max(float((np.abs(o[i:i + 1] - r) / oracle.tolerance_sparse(m)).max()) for i, (r, m) in refs.items())
+    conv.compact(x)
+    t = dev_time_us(lambda: conv.gather(shp.n, out), reps=10)
+    res.append((t, os.environ["SC_JIT_FORCE"], worst, conv.variant[1]))
+    print(f"{os.environ['SC_JIT_FORCE']:28s} gather {t:8.1f} us  err/tol {worst:.3f}  {conv.variant[1]}", flush=True)
+    del conv
+os.environ.pop("SC_JIT_FORCE", None)
+print("---- best")
+for t, p, wv, n in sorted(res)[:12]:
+    print(f"{p:28s} {t:8.1f} us err/tol {wv:.3f}")
