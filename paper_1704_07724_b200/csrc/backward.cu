@@ -36,8 +36,9 @@
 namespace sc {
 namespace bwd {
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 16;               // compute warps (one input channel each)
 constexpr int kThreads = kWarps * 32;
+constexpr int kBlock = kThreads + 32;    // + one producer warp (TMA issue in bulk mode)
 
 struct Args {
     const uint2* plist;     // [N*C][H*W] (bits, i*W + j), row-major order
@@ -54,9 +55,17 @@ struct Args {
     int tile_floats;        // shared memory: tiles, then (dgrad) one H*W dz plane per warp, then 2 mbarriers
 };
 
+template <bool B>
+struct bool_const {
+    static constexpr bool value = B;
+};
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
     asm volatile(
@@ -117,7 +126,7 @@ __device__ __forceinline__ void stage(const Args& a, float* tile, int n, int g, 
 }
 
 template <int R, int S, int KL, int T, bool WGRAD>
-__global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
+__global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
     extern __shared__ __align__(16) float smem[];
     constexpr int KC = 32 * KL;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -125,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
     float* dzbuf = smem + a.tile_floats + warp * a.H * a.W;  // dgrad: this warp's dz plane of the current image
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.tile_floats + kWarps * a.H * a.W + 2);
     full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 15) & ~(uintptr_t)15);
+    uint64_t* empty = full + 2;  // bulk mode: buffer b released by all compute warps
     // block -> (split, cblock, kc (wgrad), group)
     int b = blockIdx.x;
     const int split = b % a.splits;
@@ -137,8 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
         b /= a.kchunks;
     }
     const int g = b;
+    const bool producer = warp == kWarps;
     const int cl = cb * kWarps + warp;  // channel in group
-    const bool active = cl < a.Cg;
+    const bool active = !producer && cl < a.Cg;
     const int c = g * a.Cg + cl;
     const int n0 = split * a.ipc;
     const int n1 = min(a.n, n0 + a.ipc);
@@ -163,13 +174,29 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
         const float* src = a.dout + ((int64_t)n * a.K + (int64_t)g * a.Kg + (int64_t)kc * KC) * HoWo;
         bulk_g2s(smem + (it & 1) * KC * HoWo, src, (unsigned)(rows * HoWo * 4), full + (it & 1));
     };
-    if (a.bulk && threadIdx.x == 0) {
-        mbar_init(full, 1);
-        mbar_init(full + 1, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        issue(0);
+    if (a.bulk) {
+        // the buffers start zeroed: rows of padding filters (k >= Kg, never copied) read as 0
+        // or as an earlier tile's finite dout values, which meet only zero weights (dgrad) or
+        // accumulators that are never written out (wgrad)
+        for (int e = threadIdx.x; e < 2 * KC * HoWo; e += kBlock) smem[e] = 0.f;
+        if (threadIdx.x == 0) {
+            mbar_init(full, 1);
+            mbar_init(full + 1, 1);
+            mbar_init(empty, kWarps);
+            mbar_init(empty + 1, kWarps);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (producer) {  // tile it+2 refills buffer it&1 once all compute warps released tile it
+            if (lane == 0)
+                for (int it = 0; it < ntiles; ++it) {
+                    if (it >= 2) mbar_wait(empty + (it & 1), (unsigned)(((it >> 1) - 1) & 1));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(it);
+                }
+            return;
+        }
     }
-    if (a.bulk) __syncthreads();  // barriers initialised before anyone waits
     for (int it = 0; it < ntiles; ++it) {
         const int n = n0 + it / per_img;
         const int rem = it - (it / per_img) * per_img;
@@ -179,24 +206,18 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
         int PS;
         float* tile;
         if (a.bulk) {
-            if (it > 0) __syncthreads();  // everyone is done with tile it-1: its buffer takes tile it+1
-            if (threadIdx.x == 0 && it + 1 < ntiles) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(it + 1);
-            }
             PS = HoWo;  // odd (bwd_geometry)
             tile = smem + (it & 1) * KC * HoWo;
-            mbar_wait(full + (it & 1), (unsigned)((it >> 1) & 1));
-            const int rows = min(KC, a.Kg - kc * KC);
-            if (rows < KC) {  // padding filters read as zero
-                for (int e = threadIdx.x; e < (KC - rows) * HoWo; e += kThreads) tile[rows * HoWo + e] = 0.f;
-                __syncthreads();
+            if (it >= 1) {  // done with tile it-1: the producer may refill its buffer with tile it+1
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + ((it - 1) & 1));
             }
+            mbar_wait(full + (it & 1), (unsigned)((it >> 1) & 1));
         } else {
             if (it > 0) __syncthreads();  // everyone is done with the previous tile
             PS = ((y1 - y0) * a.Wo) | 1;  // odd k-row stride of this tile
             tile = smem;
-            stage<KL>(a, tile, n, g, kc, y0, y1 - y0, PS);
+            if (!producer) stage<KL>(a, tile, n, g, kc, y0, y1 - y0, PS);
             __syncthreads();
         }
         if (!active) continue;
@@ -251,30 +272,38 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const Args a) {
             // (ip - y0 - r)*Wo + (jp - t)
             const float* abase = tile + lane * PS + (ip - y0) * a.Wo + jp;
             float part = 0.f;
-            // branch-free taps: a tap outside the band / plane loads nothing and adds v*0 or W*0,
-            // so every tap's loads can be issued ahead of the FMAs
+            // interior nonzeros (every tap reaches the band and the plane) take an unpredicated copy
+            // of the tap loop; the others a branch-free one where a tap outside loads nothing and
+            // adds v*0 or W*0 -- in both, all taps' loads can be issued ahead of the FMAs
+            auto taps = [&](auto all) {
+                constexpr bool kAll = decltype(all)::value;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
+                for (int r = 0; r < R; ++r) {
 #pragma unroll
-                for (int t = 0; t < S; ++t) {
-                    const bool ok = ((rmask >> r) & (tmask >> t) & 1u) != 0u;
-                    const float* src;
-                    if constexpr (T == 1)
-                        src = abase - r * a.Wo - t;
-                    else
-                        src = tile + lane * PS + ((ip - r) / T - y0) * a.Wo + (jp - t) / T;
-                    float d[KL];
-#pragma unroll
-                    for (int q = 0; q < KL; ++q) d[q] = ok ? src[32 * q * PS] : 0.f;
-#pragma unroll
-                    for (int q = 0; q < KL; ++q) {
-                        if constexpr (WGRAD)
-                            acc[r * S + t][q] = fmaf(v, d[q], acc[r * S + t][q]);
+                    for (int t = 0; t < S; ++t) {
+                        const bool ok = kAll || ((rmask >> r) & (tmask >> t) & 1u) != 0u;
+                        const float* src;
+                        if constexpr (T == 1)
+                            src = abase - r * a.Wo - t;
                         else
-                            part = fmaf(wr[r * S + t][q], d[q], part);
+                            src = tile + lane * PS + ((ip - r) / T - y0) * a.Wo + (jp - t) / T;
+                        float d[KL];
+#pragma unroll
+                        for (int q = 0; q < KL; ++q) d[q] = ok ? src[32 * q * PS] : 0.f;
+#pragma unroll
+                        for (int q = 0; q < KL; ++q) {
+                            if constexpr (WGRAD)
+                                acc[r * S + t][q] = fmaf(v, d[q], acc[r * S + t][q]);
+                            else
+                                part = fmaf(wr[r * S + t][q], d[q], part);
+                        }
                     }
                 }
-            }
+            };
+            if (T == 1 && rmask == (1u << R) - 1u && tmask == (1u << S) - 1u)
+                taps(bool_const<true>{});
+            else
+                taps(bool_const<false>{});
             if constexpr (!WGRAD) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -341,7 +370,7 @@ cudaError_t launch_rs(const Args& a, int G, bool wgrad, size_t smem, cudaStream_
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.splits * a.cblocks * (wgrad ? a.kchunks : 1) * G;
-    kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
+    kern<<<(unsigned)grid, kBlock, smem, st>>>(a);
     return cudaGetLastError();
 }
 
