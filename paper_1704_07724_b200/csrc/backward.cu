@@ -27,8 +27,9 @@
 // The branch per tap is warp-uniform (all lanes share the nonzero).
 // wgrad: grid (split of images, cblock, kc, group); partial dW per split into
 // a workspace, summed in split order by bwd_reduce_kernel (deterministic).
-// dgrad: grid (split of images, cblock, group); tiles walk (n, kc, band); the
-// warp zero-fills its plane before the first tile of an image.
+// dgrad: grid (split of images, cblock, group); tiles walk (kc, n, band); per
+// (n, kc) the warp accumulates its channel's plane in shared memory and then
+// stores it (kc = 0) or adds it (kc > 0, in k-chunk order) to dz.
 #include <cuda_runtime.h>
 
 #include "sc_internal.h"
@@ -167,9 +168,24 @@ __global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
     int wr_kc = -1;
 
     // bulk mode: tile `it` (image n, chunk kc) is dout[n][g*Kg + kc*KC ..][all pixels], contiguous
+    // tile order: wgrad (image, band); dgrad (k-chunk, image, band) -- k-chunk major, so a warp
+    // reloads its channel's weights once per k-chunk, not once per tile
+    auto decode = [&](int it, int& n, int& kc, int& band) {
+        if constexpr (WGRAD) {
+            n = n0 + it / a.bands;
+            kc = kc_fixed;
+            band = it - (it / a.bands) * a.bands;
+        } else {
+            const int per_kc = (n1 - n0) * a.bands;
+            kc = it / per_kc;
+            const int rem = it - kc * per_kc;
+            n = n0 + rem / a.bands;
+            band = rem - (rem / a.bands) * a.bands;
+        }
+    };
     auto issue = [&](int it) {
-        const int n = n0 + it / per_img;
-        const int kc = WGRAD ? kc_fixed : it - (it / per_img) * per_img;
+        int n, kc, band;
+        decode(it, n, kc, band);
         const int rows = min(KC, a.Kg - kc * KC);
         const float* src = a.dout + ((int64_t)n * a.K + (int64_t)g * a.Kg + (int64_t)kc * KC) * HoWo;
         bulk_g2s(smem + (it & 1) * KC * HoWo, src, (unsigned)(rows * HoWo * 4), full + (it & 1));
@@ -198,10 +214,8 @@ __global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
         }
     }
     for (int it = 0; it < ntiles; ++it) {
-        const int n = n0 + it / per_img;
-        const int rem = it - (it / per_img) * per_img;
-        const int kc = WGRAD ? kc_fixed : rem / a.bands;
-        const int band = WGRAD ? rem : rem - (rem / a.bands) * a.bands;
+        int n, kc, band;
+        decode(it, n, kc, band);
         const int y0 = band * a.BY, y1 = min(a.Ho, y0 + a.BY);
         int PS;
         float* tile;
@@ -223,7 +237,7 @@ __global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
         if (!active) continue;
         const int64_t plane = (int64_t)n * a.C + c;
         if constexpr (!WGRAD) {
-            if (kc == 0 && band == 0) {  // first tile of this image: the plane starts at zero
+            if (band == 0) {  // first band of (image, k-chunk): this chunk's partial plane starts at zero
                 for (int e = lane; e < HW; e += 32) dzbuf[e] = 0.f;
                 __syncwarp();
             }
@@ -312,10 +326,13 @@ __global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
         }
         }
         if constexpr (!WGRAD) {
-            if (kc == a.kchunks - 1 && band == a.bands - 1) {  // last tile of this image: write the plane
+            if (band == a.bands - 1) {  // last band: store (first k-chunk) or add (later ones, in order)
                 __syncwarp();
                 float* dzp = a.dz + plane * HW;
-                for (int e = lane; e < HW; e += 32) dzp[e] = dzbuf[e];
+                if (kc == 0)
+                    for (int e = lane; e < HW; e += 32) dzp[e] = dzbuf[e];
+                else
+                    for (int e = lane; e < HW; e += 32) dzp[e] += dzbuf[e];
             }
         }
     }
