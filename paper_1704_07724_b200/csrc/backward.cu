@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(kBlock, 1) bwd_kernel(const Args a) {
                 for (int q = 0; q < KL; ++q) {
                     const int kl = kc * KC + lane + 32 * q;
                     const bool ok = kl < a.Kg;
-                    const int kb = ok ? kl / a.kbw : 0, kk = ok ? kl - kb * a.kbw : 0;
+                    const int kb = ok ? kl / a.kbw : 0, kx = ok ? kl - kb * a.kbw : 0;
+                    // position of filter kx inside a packed k-block (pack.cu: KL=3 blocks store the
+                    // pair (3l, 3l+1) at 2l and the single 3l+2 at 64 + l)
+                    const int kk = a.kbw == 96 ? (kx % 3 < 2 ? 2 * (kx / 3) + kx % 3 : 64 + kx / 3) : kx;
                     const float* wp = a.wpack + (((int64_t)g * a.fkblocks + kb) * a.Cg + cl) * (R * S) * a.kbw + kk;
 #pragma unroll
                     for (int u = 0; u < R * S; ++u) wr[u][q] = ok ? __ldg(wp + u * a.kbw) : 0.f;

@@ -215,7 +215,7 @@ std::string gen_variant(const Params& p, const std::string& sname, const std::st
         {"R", R}, {"S", S}, {"P", P}, {"T", T}, {"W", W}, {"WO", WO}, {"NX", NX}, {"TY", TY}, {"KL", KL},
         {"NW", p.NW}, {"MINB", p.MINB}, {"NWR", NWR}, {"NCASES", NCASES}, {"CH", p.CH}, {"STAGES", p.STAGES},
         {"ID", p.id}, {"NPAIR", NPAIR}, {"NSING", NSING}, {"NWP", (int)wp.size()},
-        {"NWS", ws.empty() ? 1 : (int)ws.size()}, {"SLOTS", p.SLOTS}, {"PIECE", p.PIECE}};
+        {"NWS", ws.empty() ? 1 : (int)ws.size()}, {"SLOTS", p.SLOTS}, {"PIECE", p.PIECE}, {"KMIN", 0}};
     for (auto& c : consts) line(std::string("    static constexpr int ") + c.first + " = " + std::to_string(c.second) + ";");
     line(std::string("    static constexpr bool XPAIR = ") + (XPAIR ? "true" : "false") + ";");
     line("    static constexpr const char* NAME = \"" + name + "\";");

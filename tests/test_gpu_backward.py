@@ -206,3 +206,19 @@ def test_backward_full_config_sampled(sc, cfg, s):
     ref = oracle.conv_backward_fp64(x[:, :1], w[:, :1], d, shp.stride, shp.pad, 1, want_mass=False)
     tolb = gamma(m_b) * np.abs(d.astype(np.float64)).sum(axis=(0, 2, 3)) + 1e-30
     assert np.all(np.abs(db - ref["dbias"]) <= tolb)
+
+
+@pytest.mark.parametrize("variant", [10, 12, 7, 1])
+def test_backward_with_every_weight_packing(sc, variant, monkeypatch):
+    """The backward reads the forward's packed weights: k-blocks of 32*KL with KL = 3 (V10,
+    permuted pair/single layout), 4 (V12), 1 (V7) and 2 (V1) must all give the same gradients."""
+    monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
+    shp = datagen.C2.with_batch(2)
+    x = datagen.activations(shp, 0.9, seed=12)
+    w, b = datagen.weights(shp, seed=12)
+    d = dout_for(shp, 2, 12)
+    conv = make_conv(sc, shp, w, b)
+    assert conv.variant[0] == variant
+    got = run_bwd(conv, x, d)
+    ref = oracle.conv_backward_fp64(x, w, d, shp.stride, shp.pad, shp.groups)
+    check_all(got, ref, shp, 2, 2, d)

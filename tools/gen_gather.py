@@ -56,14 +56,17 @@ VARIANTS = [
     (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
     (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
     # paper Table 2 shapes: stride 2, 1x1, small planes
-    (40, "r5s5p1t2_w11_ty5_kl2", 5, 5, 1, 11, 5, 2, 11, 1, 8, 2, None, 3, 254, 2),  # LeNet-Conv2 (T=2)
-    (41, "r5s5p2_w6_ty6_kl2", 5, 5, 2, 6, 6, 2, 11, 1, 8, 2),                       # AlexNetC-Conv3
-    (42, "r3s3p1_w5_ty5_kl4", 3, 3, 1, 5, 5, 4, 11, 1, 16, 2),                      # AlexNetI-Conv4
-    (43, "r1s1p0_w14_ty2_kl4", 1, 1, 0, 14, 2, 4, 11, 1, 32, 2),                    # Inception4a.1/.2
-    (44, "r3s3p1_w14_ty2_kl4", 3, 3, 1, 14, 2, 4, 11, 1, 16, 2),                    # Inception4e.3
-    (45, "r1s1p0_w7_ty3_kl4", 1, 1, 0, 7, 3, 4, 11, 1, 32, 2),                      # Inception5a.1/.2
-    (46, "r3s3p1_w7_ty3_kl4", 3, 3, 1, 7, 3, 4, 11, 1, 16, 2),                      # Inception5b.3
-    (47, "r5s5p2_w7_ty5_kl2", 5, 5, 2, 7, 5, 2, 11, 1, 8, 2),                       # Inception5b.5
+    # (parameters from tools/jit_tune.py sweeps of run-time generated variants, profiles/r1_jit_tune_t2.txt)
+    (40, "r5s5p1t2_w11_ty2_kl2_sl2p126", 5, 5, 1, 11, 2, 2, 11, 1, 16, 2, None, 2, 126, 2),  # LeNet-Conv2 (T=2)
+    (41, "r5s5p2_w6_ty1_kl1_s3sl2p126", 5, 5, 2, 6, 1, 1, 11, 1, 16, 3, None, 2, 126),     # AlexNetC-Conv3
+    (42, "r3s3p1_w5_ty3_kl2_sl2", 3, 3, 1, 5, 3, 2, 11, 1, 16, 2, None, 2, 254),           # AlexNetI-Conv4
+    (48, "r1s1p0_w14_ty3_kl3_sl2_k150", 1, 1, 0, 14, 3, 3, 11, 1, 16, 2, None, 2, 254, 1, 150),  # Inception4a.1
+    (43, "r1s1p0_w14_ty2_kl4", 1, 1, 0, 14, 2, 4, 11, 1, 32, 2),                           # Inception4a.2
+    (44, "r3s3p1_w14_ty3_kl2_s3sl2", 3, 3, 1, 14, 3, 2, 11, 1, 16, 3, None, 2, 254),       # Inception4e.3
+    (49, "r1s1p0_w7_ty2_kl4_s3p510_k200", 1, 1, 0, 7, 2, 4, 11, 1, 16, 3, None, 3, 510, 1, 200),  # Inception5a.1
+    (45, "r1s1p0_w7_ty2_kl2_sl2", 1, 1, 0, 7, 2, 2, 11, 1, 16, 2, None, 2, 254),           # Inception5a.2
+    (46, "r3s3p1_w7_ty2_kl4_p126", 3, 3, 1, 7, 2, 4, 11, 1, 16, 2, None, 3, 126),          # Inception5b.3
+    (47, "r5s5p2_w7_ty2_kl2_sl2p126", 5, 5, 2, 7, 2, 2, 11, 1, 16, 2, None, 2, 126),       # Inception5b.5
     (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),        # C4b
 ]
 
@@ -74,10 +77,10 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4, 33, 3]
+PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4, 33, 3, 48, 49]  # 48/49 need Kg >= KMIN
 
 
-def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1):
+def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):
     WO = (W + 2 * P - S) // T + 1
     XPAIR = KL == 1
     assert not (XPAIR and T != 1), "x-pair tiles assume stride 1"
@@ -271,7 +274,7 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
     for k, v in (("R", R), ("S", S), ("P", P), ("T", T), ("W", W), ("WO", WO), ("NX", NX), ("TY", TY), ("KL", KL),
                  ("NW", NW), ("MINB", MINB), ("NWR", NWR), ("NCASES", NCASES), ("CH", CH), ("STAGES", STAGES), ("ID", vid),
                  ("NPAIR", NPAIR), ("NSING", NSING), ("NWP", len(wp)), ("NWS", max(1, len(ws))),
-                 ("SLOTS", SLOTS), ("PIECE", PIECE)):
+                 ("SLOTS", SLOTS), ("PIECE", PIECE), ("KMIN", KMIN)):
         lines.append(f"    static constexpr int {k} = {v};")
     lines.append(f"    static constexpr bool XPAIR = {'true' if XPAIR else 'false'};")
     lines.append(f'    static constexpr const char* NAME = "{name}";')

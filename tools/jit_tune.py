@@ -16,7 +16,10 @@ from tools.probe_run import dev_time_us  # noqa: E402
 
 cfg, s = sys.argv[1], float(sys.argv[2])
 quick = len(sys.argv) > 3
-shp = datagen.CONFIGS[cfg]
+if cfg.startswith("T2:"):  # a paper Table 2 layer by name, N=128
+    shp = {t.name: t for t, _ in datagen.table2_shapes(n=128)}[cfg[3:]]
+else:
+    shp = datagen.CONFIGS[cfg]
 w, b = datagen.weights(shp)
 xh = datagen.activations(shp, s)
 x = torch.from_numpy(xh).cuda()
@@ -24,13 +27,22 @@ refs = {i: oracle.conv_fp64(xh[i:i + 1], w, b, shp.stride, shp.pad, shp.groups) 
 out = torch.empty((shp.n, shp.k, shp.ho, shp.wo), device="cuda")
 
 grid = [(2, 4), (1, 4), (2, 2), (3, 2), (4, 2), (2, 3), (3, 3)]
-if shp.k // shp.groups <= 64 and shp.stride == 1:  # few filters: x-pair tiles (KL=1) too
+if shp.k // shp.groups <= 64 and shp.stride == 1 and shp.s >= 2:  # few filters: x-pair tiles (KL=1) too
     grid += [(2, 1), (4, 1), (7, 1), (1, 1)]
+grid += [(5, 2), (6, 2), (7, 2), (5, 4), (4, 4)]
+grid = [(ty, kl) for ty, kl in grid if ty <= shp.ho]
 nws = [11, 9] if not quick else [11]
 chs = [16, 32, 8] if not quick else [16]
 stages = [2, 3]
 slots = [3, 4, 2]
 pieces = [254, 510, 126]
+full = cfg.startswith("T2:")  # Table 2 layers: time the whole forward (the tile height changes stage 1 too)
+os.environ.pop("SC_JIT_FORCE", None)
+base = sc.SparseConv(torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), shp.n, shp.c, shp.h, shp.w,
+                     shp.stride, shp.pad, shp.groups)
+tb = dev_time_us(lambda: base.forward(x, out), reps=10) if full else None
+print("shipped", base.variant, f"forward {tb:.1f} us" if tb else "", flush=True)
+del base
 res = []
 for (ty, kl), nw, ch, st, sl, pc in itertools.product(grid, nws, chs, stages, slots, pieces):
     os.environ["SC_JIT_FORCE"] = f"{ty},{kl},{nw},1,{ch},{st},{sl},{pc}"
@@ -46,8 +58,11 @@ for (ty, kl), nw, ch, st, sl, pc in itertools.product(grid, nws, chs, stages, sl
     torch.cuda.synchronize()
     o = out.cpu().numpy()
     worst = max(float((np.abs(o[i:i + 1] - r) / oracle.tolerance_sparse(m)).max()) for i, (r, m) in refs.items())
-    conv.compact(x)
-    t = dev_time_us(lambda: conv.gather(shp.n, out), reps=10)
+    if full:
+        t = dev_time_us(lambda: conv.forward(x, out), reps=10)
+    else:
+        conv.compact(x)
+        t = dev_time_us(lambda: conv.gather(shp.n, out), reps=10)
     res.append((t, os.environ["SC_JIT_FORCE"], worst, conv.variant[1]))
     print(f"{os.environ['SC_JIT_FORCE']:28s} gather {t:8.1f} us  err/tol {worst:.3f}  {conv.variant[1]}", flush=True)
     del conv
