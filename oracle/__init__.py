@@ -216,9 +216,11 @@ def stream_format(c, h, w, r, stride, pad, ty, ho):
 
 def compact_streams(x, r, stride, pad, ty):
     """P:123 step 1.  x float32 [N][C][H][W] -> dict(entries u32 [N][tiles][cap][2],
-    offs u32 [N][tiles][C+1], tiles, nwr, nwin, cap).  Each channel's marker is
-    (c, NWIN + mask) with bit r of mask set iff one of its entries sits at a
-    window row wi with wi - r = ty*stride, 0 <= ty < ty_tile (R9).  Entries
+    offs u32 [N][tiles][C+1], tiles, nwr, nwin, cap).  Each channel with at
+    least one entry in the window gets a marker (c, NWIN + mask) with bit r of
+    mask set iff one of its entries sits at a window row wi with
+    wi - r = ty*stride, 0 <= ty < ty_tile; channels without entries get none
+    (offs[c] == offs[c+1]) (R9).  Entries
     beyond offs[..][C] are left zero here and are never compared."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n, c, h, w = x.shape
@@ -246,7 +248,9 @@ def decompress_streams(st, shape, stride, pad):
             of = st["offs"][ni, t]
             for ci in range(c):
                 a, b = int(of[ci]), int(of[ci + 1])
-                assert e[a, 0] == ci and e[a, 1] >= st["nwin"], "bad channel marker"
+                if a == b:
+                    continue  # no entry in this window: no marker (R9)
+                assert b > a + 1 and e[a, 0] == ci and e[a, 1] >= st["nwin"], "bad channel marker"
                 code = e[a + 1:b, 1].astype(np.int64)
                 rows = i_lo + code // w
                 out[ni, ci, rows * w + code % w] = e[a + 1:b, 0]

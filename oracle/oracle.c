@@ -107,14 +107,15 @@ int oracle_conv_fp64(const float *in, const float *w, const float *bias,
  * i_lo = t*TY*T - P .. i_lo + NWR - 1 with NWR = (TY-1)*T + R, all W columns,
  * NWIN = NWR*W window positions.  stream[n][t] is a sequence of 8-byte
  * entries (a, b) (u32 pairs):
- *   for c = 0..C-1 (ascending):
+ *   for c = 0..C-1 (ascending) with at least one entry in the window:
  *     marker  (a = c, b = NWIN + mask), bit r of mask set iff some entry
  *             below lies at a window row wi with wi - r = ty*T for a tile
  *             row 0 <= ty < TY (the filter rows r the channel reaches)
  *     for every input x = in[n,c,i,j] != 0.0f (IEEE compare: -0.0 is zero;
  *     subnormal/NaN/Inf are nonzero) with i inside the window and the plane,
  *     ascending (i, j):  (a = bit copy of x, b = (i - i_lo)*W + j)
- *   offs[n][t][c] = index of channel c's marker, offs[n][t][C] = length.
+ *   offs[n][t][c] = index of channel c's marker (channels without entries
+ *   have none: offs[n][t][c] == offs[n][t][c+1]), offs[n][t][C] = length.
  * entries: u32 [N][tiles][cap][2]; offs: u32 [N][tiles][C+1].  Entries beyond
  * the length are not written.  Returns 0, or -1 on invalid arguments / overflow.
  */
@@ -158,7 +159,10 @@ int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int
                         }
                     }
                 }
-                st[2 * marker + 1] = (uint32_t)NWIN + mask;
+                if (len == marker + 1)
+                    len = marker;  /* no entry in this window: no marker (R9) */
+                else
+                    st[2 * marker + 1] = (uint32_t)NWIN + mask;
             }
             of[C] = (uint32_t)len;
         }

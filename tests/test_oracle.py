@@ -331,6 +331,9 @@ def test_compact_streams_against_numpy_and_roundtrip(shape, r, stride, pad, ty):
                         d = wi - rr
                         if d >= 0 and d % stride == 0 and d // stride < ty:
                             mask |= 1 << rr
+                if len(vals) == 0:
+                    assert a == b  # no entry in the window: no marker (R9)
+                    continue
                 assert e[a, 0] == ci and e[a, 1] == nwin + mask
                 assert np.array_equal(e[a + 1:b, 0], vals)
                 assert np.array_equal(e[a + 1:b, 1], codes)
@@ -398,3 +401,20 @@ def test_relu_of_symmetric_tensor_half_sparse():
     assert abs(oracle.sparsity(z) - 0.5) <= 0.02
     assert np.array_equal(oracle.relu(z), z)
     assert np.all(z >= 0)
+
+
+def test_compact_streams_empty_channels_have_no_marker():
+    """R9: a channel with no nonzero inside a tile's window contributes nothing to that
+    tile's stream (offs[c] == offs[c+1]); the others keep marker + entries in order."""
+    x = np.zeros((1, 3, 6, 4), np.float32)
+    x[0, 0, 0, 1] = 1.0      # only in tile 0's window (rows -1..2 with ty=2, r=3, pad=1)
+    x[0, 2, 5, 2] = 2.0      # only in the last tile's window
+    st = oracle.compact_streams(x, 3, 1, 1, 2)
+    assert st["tiles"] == 3
+    of = st["offs"][0].astype(np.int64)
+    e = st["entries"][0]
+    assert list(of[0]) == [0, 2, 2, 2]             # tile 0: channel 0 only
+    assert e[0, 0, 0] == 0 and e[0, 1, 1] == 1 * 4 + 1
+    assert list(of[1]) == [0, 0, 0, 0]             # tile 1 (rows 1..4): empty stream
+    assert list(of[2]) == [0, 0, 0, 2]             # tile 2 (rows 3..6): channel 2 only
+    assert e[2, 0, 0] == 2 and e[2, 1, 1] == (5 - 3) * 4 + 2
