@@ -76,12 +76,14 @@ typedef struct sc_plan_s *sc_plan;
  * window_width columns, NWIN = marker_code = NWR*W positions.  Its stream
  * (stream id s = n*tiles_per_image + t) is entries[s*stream_capacity*2 ...],
  * a sequence of u32 pairs (a, b):
- *   for every input channel c ascending: the marker (a = c, b = NWIN + mask),
- *   then every input x = in[n,c,i,j] != 0.0f inside the window (ascending
+ *   for every input channel c ascending with at least one nonzero in the
+ *   window: the marker (a = c, b = NWIN + mask), then every input
+ *   x = in[n,c,i,j] != 0.0f inside the window (ascending
  *   i, j) as (a = bit copy of x, b = (i - (t*TY*stride - pad))*W + j).
  *   Bit r of mask is set iff one of the channel's entries sits at a window
  *   row wi with wi - r = ty*stride for a tile row 0 <= ty < TY (the filter
- *   rows the channel reaches; mask = 0 iff the channel has no entry).
+ *   rows the channel reaches).  Channels without a nonzero in the window have
+ *   no marker and offsets[s*(C+1) + c] == offsets[s*(C+1) + c + 1].
  * offsets[s*(C+1) + c] = index of channel c's marker, offsets[s*(C+1) + C] =
  * stream length.  Entries beyond the length are undefined. */
 typedef struct {

@@ -16,7 +16,7 @@
 // owns channels w, w+NW, ...).  In a round every lane issues all its loads
 // at once (RCH channels x KV coalesced 4-byte loads, lanes over the run), so
 // one HBM/L2 round trip covers the round; __ballot_sync masks of the loaded
-// values give the per-channel counts, a block scan of (1 + count) gives every
+// values give the per-channel counts, a block scan of (count ? 1 + count : 0) gives every
 // channel's marker index (-> offs), and the same masks place each nonzero at
 // its rank (__popc of the lower lanes) -- values are written from registers,
 // nothing is re-read.  Runs longer than 32*KV floats are handled in blocks
@@ -98,10 +98,10 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
                     cnt += __popc(__ballot_sync(0xffffffffu, x != 0.0f));
                 }
             }
-            if (lane == 0 && ch < nround) start_s[ch] = 1u + cnt;
+            if (lane == 0 && ch < nround) start_s[ch] = cnt ? 1u + cnt : 0u;  // no entry: no marker (R9)
         }
         __syncthreads();
-        // ---- block-wide exclusive scan of (1 + count) over the round's channels;
+        // ---- block-wide exclusive scan of (count ? 1 + count : 0) over the round's channels;
         // thread i owns channels RCH*i .. RCH*i + RCH-1 of the round
         {
             uint32_t a[RCH];
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(512) compact_streams_kernel(const float* __res
                     }
                 }
                 mask = __reduce_or_sync(0xffffffffu, mask);
-                if (lane == 0) st[pos0] = make_uint2((unsigned)(cb + ch), (unsigned)NWIN + mask);
+                if (lane == 0 && pos != pos0 + 1) st[pos0] = make_uint2((unsigned)(cb + ch), (unsigned)NWIN + mask);
             }
         }
         base += wsum_s[32];
@@ -220,7 +220,7 @@ static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const
 //         before row r (lane r: popc of the ballot bits below r*W), and (c)
 //         each tile's window count cnt[n][t][c] = prow[r1] - prow[r0].
 //  emit:  one CTA per (image, chunk of 32 channels).  Warp w scans tiles
-//         w, w+NW, ...: the chunk's stream base is 1 + count summed over the
+//         w, w+NW, ...: the chunk's stream base is (count ? 1 + count : 0) summed over the
 //         channels before it, a shuffle scan over the chunk's channels gives
 //         each marker index (-> offs).  Then each warp flattens, per plane,
 //         the (tile, marker / entry) writes into one work list (scan over the
@@ -329,10 +329,11 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     for (int t = warp; t < tiles; t += kPlaneWarps) {
         const uint32_t* cs = cnt + ((int64_t)n * tiles + t) * C;
         uint32_t base = 0;
-        for (int c = lane; c < c0; c += 32) base += 1u + cs[c];
+        for (int c = lane; c < c0; c += 32) base += cs[c] ? 1u + cs[c] : 0u;  // marker only with entries (R9)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
-        const uint32_t v = lane < nch ? 1u + cs[c0 + lane] : 0u;
+        const uint32_t cv = lane < nch ? cs[c0 + lane] : 0u;
+        const uint32_t v = cv ? 1u + cv : 0u;
         uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -378,7 +379,8 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
         }
         // lane t: run [a, b) of the plane's list inside tile t's window; work = marker + run
         const uint32_t a = __shfl_sync(0xffffffffu, pv[q], r0), b = __shfl_sync(0xffffffffu, pv[q], r1);
-        const uint32_t len = lane < tiles ? 1u + (r1 > r0 ? b - a : 0u) : 0u;
+        const uint32_t cnt_t = r1 > r0 ? b - a : 0u;
+        const uint32_t len = (lane < tiles && cnt_t > 0) ? 1u + cnt_t : 0u;  // no entry: no marker (R9)
         uint32_t incl = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

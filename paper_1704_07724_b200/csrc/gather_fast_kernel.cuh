@@ -183,6 +183,10 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     uint32_t iend = bnd(1);
     int issued = 0;
     auto issue_next = [&]() {
+        while (iq < nchunks && ia == iend) {  // chunks without entries (R9: no markers either) have no piece
+            ++iq;
+            iend = bnd(iq + 1 <= nchunks ? iq + 1 : nchunks);
+        }
         if (iq >= nchunks) return;
         const uint32_t b = (ia + V::PIECE < iend) ? ia + V::PIECE : iend;
         const int slot = issued % V::SLOTS;

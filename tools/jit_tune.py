@@ -14,7 +14,7 @@ import oracle  # noqa: E402
 from paper_1704_07724_b200 import datagen, sparseconv as sc  # noqa: E402
 from tools.probe_run import dev_time_us  # noqa: E402
 
-cfg, s = sys.argv[1], float(sys.argv[2])
+cfg, s = sys.argv[1], (sys.argv[2] if sys.argv[2] == "channel" else float(sys.argv[2]))
 quick = len(sys.argv) > 3
 if cfg.startswith("T2:"):  # a paper Table 2 layer by name, N=128
     shp = {t.name: t for t, _ in datagen.table2_shapes(n=128)}[cfg[3:]]
@@ -27,7 +27,7 @@ refs = {i: oracle.conv_fp64(xh[i:i + 1], w, b, shp.stride, shp.pad, shp.groups) 
 out = torch.empty((shp.n, shp.k, shp.ho, shp.wo), device="cuda")
 
 grid = [(2, 4), (1, 4), (2, 2), (3, 2), (4, 2), (2, 3), (3, 3)]
-if shp.k // shp.groups <= 64 and shp.stride == 1 and shp.s >= 2:  # few filters: x-pair tiles (KL=1) too
+if (shp.k // shp.groups <= 64 or os.environ.get("TUNE_XPAIR")) and shp.stride == 1 and shp.s >= 2:  # x-pair tiles
     grid += [(2, 1), (4, 1), (7, 1), (1, 1)]
 grid += [(5, 2), (6, 2), (7, 2), (5, 4), (4, 4)]
 grid = [(ty, kl) for ty, kl in grid if ty <= shp.ho]
