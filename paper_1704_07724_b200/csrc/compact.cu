@@ -252,18 +252,22 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const unsigned lt = (1u << lane) - 1u;
     uint2* lst = plist + (int64_t)plane * HW;
     unsigned bal[NSLOT];
+    uint32_t pc[NSLOT];
     uint32_t total = 0;
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u) {
         const bool nz = v[u] != 0.0f;  // IEEE: -0.0 is zero
         bal[u] = __ballot_sync(0xffffffffu, nz);
-        // predicated store (no branch / reconvergence per slot)
-        const uint2* dst = lst + total + __popc(bal[u] & lt);
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.global.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(dst),
-            "r"(__float_as_uint(v[u])), "r"(32u * u + lane), "r"((unsigned)nz)
-            : "memory");
-        total += __popc(bal[u]);
+        pc[u] = __popc(bal[u]);
+        if (bal[u] != 0u) {  // warp-uniform: slots without a nonzero store nothing
+            // predicated store (no branch / reconvergence per lane)
+            const uint2* dst = lst + total + __popc(bal[u] & lt);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.global.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(dst),
+                "r"(__float_as_uint(v[u])), "r"(32u * u + lane), "r"((unsigned)nz)
+                : "memory");
+        }
+        total += pc[u];
     }
     // lane r <= H: nonzeros before element r*W (the first element of row r)
     const int eb = lane * W;
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const unsigned mb = (1u << (eb & 31)) - 1u;
     uint32_t pre = 0;
 #pragma unroll
-    for (int u = 0; u < NSLOT; ++u) pre += u < sb ? __popc(bal[u]) : (u == sb ? __popc(bal[u] & mb) : 0u);
+    for (int u = 0; u < NSLOT; ++u) pre += u < sb ? pc[u] : (u == sb ? __popc(bal[u] & mb) : 0u);
     if (lane > H) pre = total;
     if (lane <= H) prow[(int64_t)plane * (H + 1) + lane] = pre;
     const int n = plane / C, c = plane - (plane / C) * C;
@@ -393,12 +397,15 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
         // marker of tile t (R9): bit r set iff a nonzero row i = i_lo + r + ty*T, 0 <= ty < TY
         const uint32_t pnext = __shfl_down_sync(0xffffffffu, pv[q], 1);
         const unsigned rowbits = __ballot_sync(0xffffffffu, lane < H && pnext > pv[q]);
+        // = OR over tile rows ty of the R occupancy bits starting at row lo + ty*T (64-bit
+        // shifts: lo >= -P > -32; rows >= 32 do not exist)
         unsigned mask_t = 0;
-        for (int r = 0; r < R; ++r)
-            for (int ty = 0; ty < TY; ++ty) {
-                const int i = lo + r + ty * T;
-                if (i >= 0 && i < H && ((rowbits >> i) & 1u)) mask_t |= 1u << r;
-            }
+        const uint64_t rb64 = (uint64_t)rowbits << 32;
+        for (int ty = 0; ty < TY; ++ty) {
+            const int sh = 32 + lo + ty * T;
+            if (sh < 64) mask_t |= (unsigned)(rb64 >> sh);
+        }
+        mask_t &= (1u << R) - 1u;
         for (uint32_t w0 = 0; w0 < wtotal; w0 += 32) {
             const uint32_t w = w0 + lane;
             // my tile: the last t with wstart[t] <= w (tiles <= 32; wstart ascending)
