@@ -178,15 +178,23 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     // Piece sequence: the range [bnd(0), bnd(nchunks)) cut at chunk
     // boundaries and every V::PIECE entries.  Issue and consume cursors walk it
     // identically; lane 0 issues the bulk copies.
-    int iq = 0;                 // issue cursor: chunk
-    uint32_t ia = bnd(0);       // issue cursor: next entry
-    uint32_t iend = bnd(1);
+    // Chunks without entries (R9: their channels have no markers either) get no piece: bit q of
+    // `filled` marks chunk q non-empty; the issue cursor jumps over the others.
+    const uint32_t dn0 = __shfl_down_sync(0xffffffffu, bnd0, 1);  // all lanes take part in every shuffle
+    const uint32_t b32 = __shfl_sync(0xffffffffu, bnd1, 0);
+    const uint32_t nb0 = lane < 31 ? dn0 : b32;                      // bnd(lane + 1)
+    const uint32_t nb1 = __shfl_down_sync(0xffffffffu, bnd1, 1);     // bnd(lane + 33)
+    const uint64_t filled = (uint64_t)__ballot_sync(0xffffffffu, lane < nchunks && nb0 > bnd0) |
+                            ((uint64_t)__ballot_sync(0xffffffffu, lane + 32 < nchunks && nb1 > bnd1) << 32);
+    auto next_filled = [&](int q) -> int {  // first non-empty chunk >= q, else nchunks
+        const uint64_t rest = q < 64 ? filled >> q : 0ull;
+        return rest ? q + __ffsll((long long)rest) - 1 : nchunks;
+    };
+    int iq = next_filled(0);    // issue cursor: chunk (non-empty or nchunks)
+    uint32_t ia = bnd(iq < nchunks ? iq : 0);        // issue cursor: next entry
+    uint32_t iend = bnd(iq < nchunks ? iq + 1 : 0);
     int issued = 0;
     auto issue_next = [&]() {
-        while (iq < nchunks && ia == iend) {  // chunks without entries (R9: no markers either) have no piece
-            ++iq;
-            iend = bnd(iq + 1 <= nchunks ? iq + 1 : nchunks);
-        }
         if (iq >= nchunks) return;
         const uint32_t b = (ia + V::PIECE < iend) ? ia + V::PIECE : iend;
         const int slot = issued % V::SLOTS;
@@ -200,8 +208,10 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
         ++issued;
         ia = b;
         if (ia == iend) {
-            ++iq;
-            iend = bnd(iq + 1 <= nchunks ? iq + 1 : nchunks);
+            iq = next_filled(iq + 1);
+            const int qq = iq < nchunks ? iq : 0;
+            ia = bnd(qq);
+            iend = bnd(qq + 1);
         }
     };
 #pragma unroll 1
