@@ -295,6 +295,9 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
     int H, int W, int TY, int T, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
     uint32_t* __restrict__ offs, Gate gate) {
+    // let stage 2 (a programmatic dependent) start its prologue; it waits for this grid's
+    // completion before it reads the streams
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (gate_closed(gate)) return;
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
     extern __shared__ uint2 rowbuf_s[];  // FROM_ROWS: [kPlaneWarps][H*W]

@@ -81,8 +81,18 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
         kg<<<(unsigned)grid, (V::NW + 1) * 32, smem, st>>>(ag);
         return cudaGetLastError();
     }
-    kern<<<(unsigned)grid, (V::NW + 1) * 32, smem, st>>>(a);
-    return cudaGetLastError();
+    // launched as a programmatic dependent of stage 1 (the emit kernel releases it early)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((V::NW + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace fast

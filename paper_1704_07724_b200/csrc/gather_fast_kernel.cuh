@@ -168,6 +168,9 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
 
     // Chunk boundaries bnd(q) = of[min(q*CH, Cg)], q <= nchunks (<= 63), held
     // two per lane and broadcast with shuffles.
+    // programmatic dependent launch: everything above overlaps the tail of stage 1; its
+    // outputs (offs, entries) are read only from here on (a no-op without the launch attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t bnd0 = __ldg(&of[(lane * CH < a.Cg) ? lane * CH : a.Cg]);
     const uint32_t bnd1 = __ldg(&of[((lane + 32) * CH < a.Cg) ? (lane + 32) * CH : a.Cg]);
     auto bnd = [&](int q) -> uint32_t {
