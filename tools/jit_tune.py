@@ -28,9 +28,11 @@ out = torch.empty((shp.n, shp.k, shp.ho, shp.wo), device="cuda")
 
 grid = [(2, 4), (1, 4), (2, 2), (3, 2), (4, 2), (2, 3), (3, 3)]
 if (shp.k // shp.groups <= 64 or os.environ.get("TUNE_XPAIR")) and shp.stride == 1 and shp.s >= 2:  # x-pair tiles
-    grid += [(2, 1), (4, 1), (7, 1), (1, 1)]
+    grid += [(2, 1), (3, 1), (4, 1), (5, 1), (6, 1), (7, 1), (1, 1)]
 grid += [(5, 2), (6, 2), (7, 2), (5, 4), (4, 4)]
 grid = [(ty, kl) for ty, kl in grid if ty <= shp.ho]
+if os.environ.get("TUNE_ONLY_XPAIR"):
+    grid = [(ty, kl) for ty, kl in grid if kl == 1]
 nws = [11, 9] if not quick else [11]
 chs = [16, 32, 8] if not quick else [16]
 stages = [2, 3]
