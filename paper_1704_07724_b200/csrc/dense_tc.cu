@@ -99,6 +99,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // dimension must be a multiple of 16 bytes).
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                           int C, int Cp, int Cg, int Cgp, int HW, Gate gate) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the GEMM's prologue may start
     if (gate_closed(gate)) return;
     __shared__ float tile[32][33];
     const int n = blockIdx.z;
@@ -165,6 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     if (warp == kTmaWarp) {
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+            // programmatic dependent of the transpose: its output is read from here on
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             const float* asrc = a.adense + ((size_t)g * a.mtiles + mt) * nk * (kATileBytes / 4);
             const unsigned bbytes = (unsigned)(a.npix * BK * 4);
             for (int kb = 0; kb < nk; ++kb) {
@@ -373,8 +376,19 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     const long long grid = (long long)n * g.G * dg.mtiles * dg.ptiles;
     CUtensorMap map;
     memcpy(&map, map128, sizeof(map));
-    dense_tc_kernel<<<(unsigned)grid, kThreads, smem, st>>>(map, a);
-    return cudaGetLastError();
+    // launched as a programmatic dependent of the transpose (TMEM allocation and barrier setup
+    // overlap its tail)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, dense_tc_kernel, map, a);
 }
 
 }  // namespace sc
