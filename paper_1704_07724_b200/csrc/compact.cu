@@ -4,9 +4,10 @@
 // and store the non-zero values in a vector with their column and row
 // information".  Output format: reading R9 (include/sparse_conv.h,
 // DESIGN.md): one stream per (image n, output row-tile t) holding, for every
-// input channel c in order, a marker (c, NWIN + mask) followed by the channel's
-// nonzeros inside the tile's input window as (value bits, window position),
-// ascending; offs[n][t][c] = index of channel c's marker, offs[..][C] = length;
+// input channel c in order that has a nonzero inside the tile's input window, a
+// marker (c, NWIN + mask) followed by those nonzeros as (value bits, window
+// position), ascending; offs[n][t][c] = index of channel c's marker (channels
+// without entries have none: offs[c] == offs[c+1]), offs[..][C] = length;
 // bit r of mask = filter row r is reached by one of the channel's entries.
 // The stream is exactly the instruction stream the stage-2 interpreter runs.
 //
