@@ -46,6 +46,7 @@ struct Args {
     int rows, ptiles, mtiles, cb, kblocks, npix, nmma, cgp;
     uint32_t idesc;
     Gate gate;
+    int nitems;  // (image, group, M-tile, pixel tile) work items
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -56,6 +57,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
     asm volatile(
@@ -98,29 +102,43 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // keeps every group's first channel 16-byte aligned (a TMA box start in the channel
 // dimension must be a multiple of 16 bytes).
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                          int C, int Cp, int Cg, int Cgp, int HW, Gate gate) {
+                                                          int C, int Cp, int Cg, int Cgp, int HW, int nimg,
+                                                          Gate gate) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the GEMM's prologue may start
     if (gate_closed(gate)) return;
     __shared__ float tile[32][33];
-    const int n = blockIdx.z;
-    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    // grid-stride over (pixel block, channel block, image) tiles: a bounded grid keeps a
+    // gated-off launch (device-side crossover) to a few waves of CTAs that exit at once
+    const int pblocks = (HW + 31) / 32, cblocks = (Cp + 31) / 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    const float* src = in + (size_t)n * C * HW;
+    for (int tid = blockIdx.x; tid < pblocks * cblocks * nimg; tid += gridDim.x) {
+        const int pb = tid % pblocks, rest = tid / pblocks;
+        const int cbk = rest % cblocks, n = rest / cblocks;
+        const int p0 = pb * 32, c0 = cbk * 32;
+        const float* src = in + (size_t)n * C * HW;
 #pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-        const int oc = c0 + ty + i, p = p0 + tx;  // output channel oc = g*Cgp + cl
-        const int g = oc / Cgp, cl = oc - g * Cgp;
-        tile[ty + i][tx] = (oc < Cp && cl < Cg && p < HW) ? to_tf32(__ldg(src + (size_t)(g * Cg + cl) * HW + p)) : 0.f;
-    }
-    __syncthreads();
-    float* dst = out + (size_t)n * HW * Cp;
+        for (int i = 0; i < 32; i += 8) {
+            const int oc = c0 + ty + i, p = p0 + tx;  // output channel oc = g*Cgp + cl
+            const int g = oc / Cgp, cl = oc - g * Cgp;
+            tile[ty + i][tx] =
+                (oc < Cp && cl < Cg && p < HW) ? to_tf32(__ldg(src + (size_t)(g * Cg + cl) * HW + p)) : 0.f;
+        }
+        __syncthreads();
+        float* dst = out + (size_t)n * HW * Cp;
 #pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-        const int p = p0 + ty + i, c = c0 + tx;
-        if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][ty + i];
+        for (int i = 0; i < 32; i += 8) {
+            const int p = p0 + ty + i, c = c0 + tx;
+            if (p < HW && c < Cp) dst[(size_t)p * Cp + c] = tile[tx][ty + i];
+        }
+        __syncthreads();
     }
 }
 
+// Persistent: CTA b walks work items it = b, b + grid, ... (item = one (image, group,
+// M-tile, pixel tile)); TMEM holds two accumulators (2 x 256 columns, allocated once),
+// so the MMAs of item j+1 run while the epilogue drains item j.  A grid of at most one
+// CTA per SM also keeps the cost of a gated-off launch (device-side crossover) to one
+// wave of CTAs that exit at once.
 __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ CUtensorMap bmap, const Args a) {
     if (gate_closed(a.gate)) return;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -129,31 +147,36 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     unsigned char* sB = smem + STAGES * kATileBytes;           // STAGES x 32 KB
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kBTileBytes);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_full = empty + STAGES;   // [2]: accumulator b ready for the epilogue
+    uint64_t* tmem_empty = tmem_full + 2;   // [2]: accumulator b drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     float* epi = reinterpret_cast<float*>(sB + STAGES * kBTileBytes + 256);  // 4 warps x 32 x 33
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int bid = blockIdx.x;
-    const int pt = bid % a.ptiles;
-    bid /= a.ptiles;
-    const int mt = bid % a.mtiles;
-    bid /= a.mtiles;
-    const int g = bid % (a.K / a.Kg);
-    const int n = bid / (a.K / a.Kg);
-    const int y0 = pt * a.rows;
+    const int G = a.K / a.Kg;
+    auto decode = [&](int it, int& n, int& g, int& mt, int& pt) {
+        pt = it % a.ptiles;
+        it /= a.ptiles;
+        mt = it % a.mtiles;
+        it /= a.mtiles;
+        g = it % G;
+        n = it / G;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols)
+                     "r"(2 * kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -168,94 +191,120 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
             // programmatic dependent of the transpose: its output is read from here on
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            const float* asrc = a.adense + ((size_t)g * a.mtiles + mt) * nk * (kATileBytes / 4);
             const unsigned bbytes = (unsigned)(a.npix * BK * 4);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-                const int rs = kb / a.cb, cb = kb - rs * a.cb;
-                const int r = rs / a.S, t = rs - r * a.S;
-                mbar_expect_tx(&full[s], kATileBytes + bbytes);
-                tma_bulk_g2s(sA + s * kATileBytes, asrc + (size_t)kb * (kATileBytes / 4), kATileBytes, &full[s]);
-                tma_load_4d(sB + s * kBTileBytes, &bmap, g * a.cgp + cb * BK, t - a.P, y0 * a.T + r - a.P, n, &full[s]);
+            int q = 0;  // K blocks issued so far (stage ring position)
+            for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+                int n, g, mt, pt;
+                decode(it, n, g, mt, pt);
+                const int y0 = pt * a.rows;
+                const float* asrc = a.adense + ((size_t)g * a.mtiles + mt) * nk * (kATileBytes / 4);
+                for (int kb = 0; kb < nk; ++kb, ++q) {
+                    const int s = q % STAGES;
+                    if (q >= STAGES) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
+                    const int rs = kb / a.cb, cb = kb - rs * a.cb;
+                    const int r = rs / a.S, t = rs - r * a.S;
+                    mbar_expect_tx(&full[s], kATileBytes + bbytes);
+                    tma_bulk_g2s(sA + s * kATileBytes, asrc + (size_t)kb * (kATileBytes / 4), kATileBytes, &full[s]);
+                    tma_load_4d(sB + s * kBTileBytes, &bmap, g * a.cgp + cb * BK, t - a.P, y0 * a.T + r - a.P, n,
+                                &full[s]);
+                }
             }
         }
     } else if (warp == kMmaWarp) {
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(&full[s], (kb / STAGES) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
-                const uint32_t abase = smem_u32(sA + s * kATileBytes);
-                const uint32_t bbase = smem_u32(sB + s * kBTileBytes);
-#pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
-                    const uint64_t ad = sw128_desc(abase + k * 32);
-                    const uint64_t bd = sw128_desc(bbase + k * 32);
-                    const uint32_t acc = (kb | k) ? 1u : 0u;
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                        "l"(ad), "l"(bd), "r"(a.idesc), "r"(acc)
-                        : "memory");
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_u32(&empty[s]))
-                             : "memory");
+        int q = 0, j = 0;
+        for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++j) {
+            const int b = j & 1;
+            if (j >= 2) {  // the epilogue has drained accumulator b (item j-2)
+                mbar_wait(&tmem_empty[b], ((j >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             }
+            for (int kb = 0; kb < nk; ++kb, ++q) {
+                const int s = q % STAGES;
+                mbar_wait(&full[s], (q / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t abase = smem_u32(sA + s * kATileBytes);
+                    const uint32_t bbase = smem_u32(sB + s * kBTileBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 8; ++k) {
+                        const uint64_t ad = sw128_desc(abase + k * 32);
+                        const uint64_t bd = sw128_desc(bbase + k * 32);
+                        const uint32_t acc = (kb | k) ? 1u : 0u;
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                                tmem + (uint32_t)(b * kTmemCols)),
+                            "l"(ad), "l"(bd), "r"(a.idesc), "r"(acc)
+                            : "memory");
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(&empty[s]))
+                                 : "memory");
+                }
+                __syncwarp();
+            }
+            if (lane == 0)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&tmem_full[b]))
+                             : "memory");
             __syncwarp();
         }
-        if (lane == 0)
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(tmem_full))
-                         : "memory");
-        __syncwarp();
     } else {
         // ---- epilogue: warps 0-3 own TMEM lanes 32w..32w+31 (= output channels) ----
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float* buf = epi + warp * 32 * 33;
-        const int m0 = mt * BM + warp * 32;
-        int valid = a.HoWo - y0 * a.Wo;  // pixels of this tile inside the image
-        if (valid > a.npix) valid = a.npix;
-        for (int c0 = 0; c0 < a.nmma; c0 += 32) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        int j = 0;
+        for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++j) {
+            const int b = j & 1;
+            int n, g, mt, pt;
+            decode(it, n, g, mt, pt);
+            const int y0 = pt * a.rows;
+            mbar_wait(&tmem_full[b], (j >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int m0 = mt * BM + warp * 32;
+            int valid = a.HoWo - y0 * a.Wo;  // pixels of this tile inside the image
+            if (valid > a.npix) valid = a.npix;
+            for (int c0 = 0; c0 < a.nmma; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * kTmemCols + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(r[j]);  // [m][pixel]
-            __syncwarp();
-            const int pix = c0 + lane;
-            if (pix < valid) {
-                float* dst = a.out + ((size_t)n * a.K + (size_t)g * a.Kg) * a.HoWo + (size_t)y0 * a.Wo + pix;
+                for (int jj = 0; jj < 32; ++jj) buf[lane * 33 + jj] = __uint_as_float(r[jj]);  // [m][pixel]
+                __syncwarp();
+                const int pix = c0 + lane;
+                if (pix < valid) {
+                    float* dst = a.out + ((size_t)n * a.K + (size_t)g * a.Kg) * a.HoWo + (size_t)y0 * a.Wo + pix;
 #pragma unroll 4
-                for (int mm = 0; mm < 32; ++mm) {
-                    const int m = m0 + mm;
-                    if (m < a.Kg) {
-                        float o = buf[mm * 33 + lane] + __ldg(&a.bias[g * a.Kg + m]);
-                        if (a.relu) o = fmaxf(o, 0.f);
-                        dst[(size_t)m * a.HoWo] = o;
+                    for (int mm = 0; mm < 32; ++mm) {
+                        const int m = m0 + mm;
+                        if (m < a.Kg) {
+                            float o = buf[mm * 33 + lane] + __ldg(&a.bias[g * a.Kg + m]);
+                            if (a.relu) o = fmaxf(o, 0.f);
+                            dst[(size_t)m * a.HoWo] = o;
+                        }
                     }
                 }
+                __syncwarp();
             }
-            __syncwarp();
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            if (lane == 0) mbar_arrive_cta(&tmem_empty[b]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols)
+                     : "memory");
     }
 }
 
@@ -353,8 +402,13 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     using namespace dense;
     if (!dg.supported) return cudaErrorNotSupported;
     const int HW = (int)(g.H * g.W);
-    dim3 tgrid((unsigned)((HW + 31) / 32), (unsigned)((dg.cp + 31) / 32), (unsigned)n);
-    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, (int)g.Cg, (int)dg.cgp, HW, gate);
+    const long long ttiles = (long long)((HW + 31) / 32) * ((dg.cp + 31) / 32) * n;
+    // one CTA per tile for the plain dense path; gated (device-side crossover) launches cap the
+    // grid, so that a launch whose work is skipped costs a few waves of exiting CTAs only
+    const long long tcap = gate.flag ? 148 * 8 : ttiles;
+    const unsigned tgrid = (unsigned)(ttiles < tcap ? ttiles : tcap);
+    nchw_to_nhwc_kernel<<<tgrid, 256, 0, st>>>(in, nhwc, (int)g.C, (int)dg.cp, (int)g.Cg, (int)dg.cgp, HW, (int)n,
+                                               gate);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     Args a;
@@ -373,7 +427,14 @@ cudaError_t launch_dense_tc(const Geometry& g, const DenseGeom& dg, int64_t n, c
     const size_t smem = 1024 + STAGES * (kATileBytes + kBTileBytes) + 256 + kEpiWarps * 32 * 33 * 4;
     e = cudaFuncSetAttribute(dense_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long long grid = (long long)n * g.G * dg.mtiles * dg.ptiles;
+    a.nitems = (int)((long long)n * g.G * dg.mtiles * dg.ptiles);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+    }
+    const long long grid = a.nitems < sms ? a.nitems : sms;  // persistent: at most one CTA per SM
     CUtensorMap map;
     memcpy(&map, map128, sizeof(map));
     // launched as a programmatic dependent of the transpose (TMEM allocation and barrier setup
