@@ -12,7 +12,7 @@ G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
 
-KEEP = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'smsp__inst_executed.sum',
+KEEP = ['gpu__time_duration.sum', 'sm__pipe_tensor', 'sm__pipe_tc', 'lts__t_bytes.sum', 'lts__throughput.avg.pct', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'smsp__inst_executed.sum',
         'launch__registers_per_thread', 'launch__grid_size', 'launch__block_size',
         'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active',
         'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active',
@@ -65,6 +65,14 @@ def main():
     summary(os.path.join(G, "compact_full.ncu-rep"),
             f"# ncu --set full --clock-control none: stage-1 compaction kernels, C2 s=0.95, B200 ({tag})\n",
             os.path.join(P, f"{tag}_compact_C2_s095_raw_summary.txt"))
+    if os.path.exists(os.path.join(G, "dense_full.ncu-rep")):
+        summary(os.path.join(G, "dense_full.ncu-rep"),
+                f"# ncu --set full --clock-control none: dense tcgen05 TF32 GEMM (persistent), C2 N=128, B200 ({tag})\n",
+                os.path.join(P, f"{tag}_dense_C2_raw_summary.txt"))
+    for src, dst in (("crossover.txt", f"{tag}_crossover_C2_C4a_C4b.txt"), ("auto_overhead.txt", f"{tag}_auto_overhead_C2.txt"),
+                     ("bench_bwd.log", f"{tag}_backward_C2.jsonl")):
+        if os.path.exists(os.path.join(G, src)) and os.path.getsize(os.path.join(G, src)) > 0:
+            shutil.copy(os.path.join(G, src), os.path.join(P, dst))
     h, u, v = g[0], g[1], g[2]
     traffic = to_bytes(u[h.index('dram__bytes_read.sum')], v[h.index('dram__bytes_read.sum')]) + \
         to_bytes(u[h.index('dram__bytes_write.sum')], v[h.index('dram__bytes_write.sum')])
