@@ -134,9 +134,11 @@ sc_status dense_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *
 /* End-to-end variant of sparse_conv_forward with HOST buffers: copies h_in
  * (n images) to plan-owned device staging, runs the sparse forward, copies the
  * result back into h_out, then synchronizes `stream`.  The batch is pipelined
- * in up to 8 chunks of whole images on plan-owned streams (copy-in of chunk i
- * overlaps the kernels of chunk i-1 and the copy-out of chunk i-2); the work
- * starts after everything already queued on `stream`.  For full copy bandwidth
+ * in up to 8 chunks of whole images on plan-owned streams: copy-ins, kernels
+ * and copy-outs of different chunks overlap, and the kernels of consecutive
+ * chunks run concurrently on two streams, each chunk in its own image slice of
+ * the plan workspace; the work starts after everything already queued on
+ * `stream`.  For full copy bandwidth
  * (and overlap) h_in/h_out should be pinned (cudaHostAlloc/register). */
 sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, float *h_out,
                                    sc_stream_t stream);

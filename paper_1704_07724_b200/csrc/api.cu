@@ -48,7 +48,8 @@ struct sc_plan_s {
     // sparse_conv_forward_host pipeline (created on first use): copy-in, compute and
     // copy-out streams, per-chunk events
     static constexpr int kHostChunks = 8;
-    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    static constexpr int kHostComp = 4;  // compute streams (chunks use disjoint workspace slices)
+    cudaStream_t hs[2 + kHostComp] = {};  // [0] copy-in, [1] copy-out, [2..] compute
     cudaEvent_t ev_in[kHostChunks] = {}, ev_comp[kHostChunks] = {}, ev_start = nullptr, ev_done = nullptr;
 };
 
@@ -230,11 +231,19 @@ cudaError_t launch_stage2(sc_plan_s* p, int64_t n, const uint2* entries, const u
 }
 
 // stage 1 + stage 2 of the sparse path (gated: f3)
+// img0: the images' slice of the plan workspace (every stage-1/stage-2 buffer is image-major), so
+// launches for disjoint image ranges may run concurrently (sparse_conv_forward_host)
 cudaError_t enqueue_sparse(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
-                           sc::Gate gate = {}) {
-    cudaError_t e = sc::launch_compact(p->g, n, d_in, p->cnt, p->plist, p->prow, p->entries, p->offs, s, gate);
+                           sc::Gate gate = {}, int64_t img0 = 0) {
+    const Geometry& g = p->g;
+    uint32_t* cnt = p->cnt ? p->cnt + img0 * g.tiles * g.C : nullptr;
+    uint2* plist = p->plist ? p->plist + img0 * g.C * g.H * g.W : nullptr;
+    uint32_t* prow = p->prow ? p->prow + img0 * g.C * (g.H + 1) : nullptr;
+    uint2* entries = p->entries + img0 * g.tiles * g.cap;
+    uint32_t* offs = p->offs + img0 * g.tiles * (g.C + 1);
+    cudaError_t e = sc::launch_compact(g, n, d_in, cnt, plist, prow, entries, offs, s, gate);
     if (e != cudaSuccess) return e;
-    return launch_stage2(p, n, p->entries, p->offs, d_out, nullptr, nullptr, s, gate);
+    return launch_stage2(p, n, entries, offs, d_out, nullptr, nullptr, s, gate);
 }
 
 cudaError_t enqueue_dense(sc_plan_s* p, int64_t n, const float* d_in, float* d_out, cudaStream_t s,
@@ -478,14 +487,19 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
     if ((e = ensure_staging(plan)) != cudaSuccess || (e = ensure_host_pipeline(plan)) != cudaSuccess)
         return cuda_fail(e, "host pipeline setup");
     cudaStream_t s = (cudaStream_t)stream;
-    cudaStream_t h2d = plan->hs[0], comp = plan->hs[1], d2h = plan->hs[2];
+    cudaStream_t h2d = plan->hs[0], d2h = plan->hs[1];
+    static const int ncomp = [] {
+        const char* v = getenv("SC_HOST_STREAMS");  // measurement knob: compute streams, 1..kHostComp
+        const int c = v ? atoi(v) : 2;
+        return c < 1 ? 1 : (c > sc_plan_s::kHostComp ? sc_plan_s::kHostComp : c);
+    }();
     const int64_t in_img = g.C * g.H * g.W, out_img = g.K * g.Ho * g.Wo;
     // chunks of whole images, boundaries at multiples of 4 images (16-byte aligned device
-    // pointers for any shape); chunk i's copy-in overlaps chunk i-1's kernels and chunk i-2's
-    // copy-out (separate copy engines for the two directions)
+    // pointers for any shape); copy-in, kernels and copy-out of different chunks overlap (separate
+    // copy engines for the two directions, kernels of consecutive chunks on different streams)
     static const int max_chunks = [] {
         const char* v = getenv("SC_HOST_CHUNKS");  // measurement knob, 1..kHostChunks
-        const int c = v ? atoi(v) : 4;
+        const int c = v ? atoi(v) : 8;
         return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
     }();
     static const int64_t first_env = [] {
@@ -508,30 +522,31 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
             bounds[i] = i == chunks ? n : ((first + (n - first) * (i - 1) / (chunks - 1)) & ~(int64_t)3);
     }
     if ((e = cudaEventRecord(plan->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
-    for (cudaStream_t x : {h2d, comp, d2h})
-        if ((e = cudaStreamWaitEvent(x, plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    for (int k = 0; k < 2 + ncomp; ++k)
+        if ((e = cudaStreamWaitEvent(plan->hs[k], plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     for (int i = 0; i < chunks; ++i) {
         const int64_t c0 = bounds[i], c1 = bounds[i + 1];
         if (c1 <= c0) continue;
         const size_t bi = sizeof(float) * (c1 - c0) * in_img, bo = sizeof(float) * (c1 - c0) * out_img;
         float* din = plan->stage_in + c0 * in_img;
         float* dout = plan->stage_out + c0 * out_img;
+        // chunk i computes on stream 2 + i % ncomp in its own workspace slice, so the kernels of
+        // consecutive chunks overlap (a small chunk fills only part of the GPU)
+        cudaStream_t comp = plan->hs[2 + i % ncomp];
         if ((e = cudaMemcpyAsync(din, h_in + c0 * in_img, bi, cudaMemcpyHostToDevice, h2d)) != cudaSuccess ||
             (e = cudaEventRecord(plan->ev_in[i], h2d)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(comp, plan->ev_in[i], 0)) != cudaSuccess)
             return cuda_fail(e, "H2D copy");
-        // kernels run in chunk order on one stream: the plan's workspace is reused chunk to chunk
-        if ((e = enqueue_sparse(plan, c1 - c0, din, dout, comp)) != cudaSuccess) return cuda_fail(e, "forward");
+        if ((e = enqueue_sparse(plan, c1 - c0, din, dout, comp, {}, c0)) != cudaSuccess) return cuda_fail(e, "forward");
         if ((e = cudaEventRecord(plan->ev_comp[i], comp)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(d2h, plan->ev_comp[i], 0)) != cudaSuccess ||
             (e = cudaMemcpyAsync(h_out + c0 * out_img, dout, bo, cudaMemcpyDeviceToHost, d2h)) != cudaSuccess)
             return cuda_fail(e, "D2H copy");
     }
     // the caller's stream resumes after everything (kernels and copies) of this call
+    // (every chunk's kernels precede its copy-out, so the copy-out stream joins them all)
     if ((e = cudaEventRecord(plan->ev_done, d2h)) != cudaSuccess ||
-        (e = cudaStreamWaitEvent(s, plan->ev_done, 0)) != cudaSuccess ||
-        (e = cudaEventRecord(plan->ev_comp[0], comp)) != cudaSuccess ||
-        (e = cudaStreamWaitEvent(s, plan->ev_comp[0], 0)) != cudaSuccess)
+        (e = cudaStreamWaitEvent(s, plan->ev_done, 0)) != cudaSuccess)
         return cuda_fail(e, "stream join");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
     return SC_OK;
