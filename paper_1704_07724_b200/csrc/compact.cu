@@ -412,12 +412,13 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
         mask_t &= (1u << R) - 1u;
         for (uint32_t w0 = 0; w0 < wtotal; w0 += 32) {
             const uint32_t w = w0 + lane;
-            // my tile: the last t with wstart[t] <= w (tiles <= 32; wstart ascending)
-            const unsigned le = __ballot_sync(0xffffffffu, lane < tiles && wstart <= w0 + 31u);
+            // my tile: the last t with wstart[t] <= w (tiles <= 32; wstart non-decreasing, wstart[0]
+            // = 0): binary search over the lanes' wstart, five shuffles whatever the tile count
             int t = 0;
-            for (unsigned m = le; m; m &= m - 1) {
-                const int tt = __ffs(m) - 1;
-                if (__shfl_sync(0xffffffffu, wstart, tt) <= w) t = tt;
+#pragma unroll
+            for (int k = 16; k > 0; k >>= 1) {
+                const uint32_t ws_k = __shfl_sync(0xffffffffu, wstart, (t + k) & 31);
+                if (t + k < tiles && ws_k <= w) t += k;
             }
             const uint32_t ws_t = __shfl_sync(0xffffffffu, wstart, t);
             const uint32_t a_t = __shfl_sync(0xffffffffu, a, t);
