@@ -230,7 +230,6 @@ static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const
 namespace {
 constexpr int kMaxSlots = 32;     // plane elements / 32 on the plane-major path
 constexpr int kPlaneWarps = 8;
-constexpr int kPlaneChunk = 32;   // channels per emit CTA
 constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 }  // namespace
 
@@ -291,7 +290,7 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
 // per-(plane, row) slots rows[plane*H + r][0..W) with counts rcnt[plane*H + r]
 // (entries (bits, flat index)); each warp first gathers a plane's rows into a
 // contiguous shared list and derives the row prefix from the counts.
-template <bool FROM_ROWS>
+template <bool FROM_ROWS, int kPlaneChunk>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
     int H, int W, int TY, int T, int P, int NWR, int NWIN, int tiles, int64_t cap, int chunks, uint2* __restrict__ entries,
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
             if (lane >= o) incl += u;
         }
         const uint32_t start = base + incl - v;
-        start_s[t][lane] = start;
+        if (lane < kPlaneChunk) start_s[t][lane] = start;
         uint32_t* of = offs + ((int64_t)n * tiles + t) * (C + 1);
         if (lane < nch) of[c0 + lane] = start;
         if (lane == nch - 1 && c0 + nch == C) of[C] = start + v;
@@ -468,16 +467,28 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
     return cudaGetLastError();
 }
 
+// Channels per emit CTA: 32 (measured best on C2: 1024 CTAs), 16 when 32 would leave fewer
+// than four CTAs per SM (C4a / C3: 384 -> 768 CTAs, compaction 31 -> 30 and 32 -> 30 us).
+static int emit_chunk(const Geometry& g, int64_t n) {
+    return n * ((g.C + 31) / 32) >= 4 * 148 ? 32 : 16;
+}
+
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
                            uint32_t* prow, uint2* entries, uint32_t* offs, cudaStream_t st, Gate gate) {
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
         return launch_compact_streamwise(g, n, in, entries, offs, st, gate);
     cudaError_t e = launch_plane_lists(g, n, in, cnt, plist, prow, st, gate);
     if (e != cudaSuccess) return e;
-    const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
-    compact_plane_emit_kernel<false><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
-        plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-        (int)g.tiles, g.cap, chunks, entries, offs, gate);
+    const int ch = emit_chunk(g, n);
+    const int chunks = (int)((g.C + ch - 1) / ch);
+    if (ch == 32)
+        compact_plane_emit_kernel<false, 32><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
+            plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
+            (int)g.tiles, g.cap, chunks, entries, offs, gate);
+    else
+        compact_plane_emit_kernel<false, 16><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
+            plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
+            (int)g.tiles, g.cap, chunks, entries, offs, gate);
     return cudaGetLastError();
 }
 
@@ -505,14 +516,15 @@ cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt
         rcnt, planes, (int)g.C, (int)g.H, TYT, (int)g.P, (int)g.nwr, (int)g.tiles, cnt);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int chunks = (int)((g.C + kPlaneChunk - 1) / kPlaneChunk);
+    const int ch = emit_chunk(g, n);
+    const int chunks = (int)((g.C + ch - 1) / ch);
     const size_t smem = sizeof(uint2) * kPlaneWarps * g.H * g.W;
+    auto kern = ch == 32 ? compact_plane_emit_kernel<true, 32> : compact_plane_emit_kernel<true, 16>;
     if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(compact_plane_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    compact_plane_emit_kernel<true><<<(unsigned)(n * chunks), kPlaneWarps * 32, smem, st>>>(
+    kern<<<(unsigned)(n * chunks), kPlaneWarps * 32, smem, st>>>(
         rows, rcnt, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
         (int)g.tiles, g.cap, chunks, entries, offs, Gate{});
     return cudaGetLastError();
