@@ -235,12 +235,15 @@ constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 
 template <int NSLOT>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
-    const float* __restrict__ in, int planes, int C, int H, int W, int TYT, int P, int NWR, int tiles,
+    const float* __restrict__ in, int nimg, int C, int H, int W, int TYT, int P, int NWR, int tiles,
     uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow, Gate gate) {
     if (gate_closed(gate)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int plane = blockIdx.x * kPlaneWarps + warp;
-    if (plane >= planes) return;
+    // grid (channel blocks, images): no division to split a plane index
+    const int c = blockIdx.x * kPlaneWarps + warp;
+    if (c >= C) return;
+    for (int n = blockIdx.y; n < nimg; n += gridDim.y) {
+    const int plane = n * C + c;
     const int HW = H * W;
     const float* src = in + (int64_t)plane * HW;
     float v[NSLOT];
@@ -275,15 +278,18 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const unsigned mb = (1u << (eb & 31)) - 1u;
     uint32_t pre = 0;
 #pragma unroll
-    for (int u = 0; u < NSLOT; ++u) pre += u < sb ? pc[u] : (u == sb ? __popc(bal[u] & mb) : 0u);
+    for (int u = 0; u < NSLOT; ++u) {  // branch-free: slots below sb whole, slot sb below element eb
+        const unsigned m = u < sb ? 0xffffffffu : (u == sb ? mb : 0u);
+        pre += __popc(bal[u] & m);
+    }
     if (lane > H) pre = total;
     if (lane <= H) prow[(int64_t)plane * (H + 1) + lane] = pre;
-    const int n = plane / C, c = plane - (plane / C) * C;
     // lane t: tile t's window rows [t*TYT - P, + NWR) clipped to the plane
     const int lo = lane * TYT - P;
     const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
     const uint32_t p0 = __shfl_sync(0xffffffffu, pre, r0), p1 = __shfl_sync(0xffffffffu, pre, r1);
     if (lane < tiles) cnt[((int64_t)n * tiles + lane) * C + c] = r1 > r0 ? p1 - p0 : 0u;
+    }
 }
 
 // FROM_ROWS (chained layers, f1): the plane lists come from the producing gather as
@@ -448,12 +454,11 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
         return cudaErrorNotSupported;
     const int TYT = (int)(g.ty * g.T);
-    const int planes = (int)(n * g.C);
-    const unsigned cgrid = (unsigned)((planes + kPlaneWarps - 1) / kPlaneWarps);
+    const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(n < 65535 ? n : 65535));
     // the smallest instantiated slot count covering the plane (loads of 32 elements)
     const int64_t slots = (g.H * g.W + 31) / 32;
 #define SC_COUNT(NS)                                                                                             \
-    compact_plane_count_kernel<NS><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, planes, (int)g.C, (int)g.H, (int)g.W, \
+    compact_plane_count_kernel<NS><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, (int)n, (int)g.C, (int)g.H, (int)g.W,  \
                                                                        TYT, (int)g.P, (int)g.nwr, (int)g.tiles,   \
                                                                        cnt, plist, prow, gate)
     if (slots <= 2) SC_COUNT(2);
