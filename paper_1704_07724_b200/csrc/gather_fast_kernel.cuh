@@ -132,7 +132,14 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
                 const int chs = (a.Cg - q * CH) < CH ? (a.Cg - q * CH) : CH;
                 const unsigned bytes = (unsigned)(chs * RS * KBW * sizeof(float));
                 mbar_expect_tx(&full[qs], bytes);
-                tma_bulk_g2s(ring + qs * SM::kStageFloats, wsrc + (size_t)q * CH * RS * KBW, bytes, &full[qs]);
+                // the stage in four bulk copies (more requests in flight than one long copy)
+                const unsigned part = ((bytes / 4u) + 15u) & ~15u;
+                for (unsigned off = 0; off < bytes; off += part) {
+                    const unsigned len = bytes - off < part ? bytes - off : part;
+                    tma_bulk_g2s(reinterpret_cast<unsigned char*>(ring + qs * SM::kStageFloats) + off,
+                                 reinterpret_cast<const unsigned char*>(wsrc + (size_t)q * CH * RS * KBW) + off, len,
+                                 &full[qs]);
+                }
             }
         }
         return;
