@@ -422,8 +422,10 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
             int t = 0;
 #pragma unroll
             for (int k = 16; k > 0; k >>= 1) {
-                const uint32_t ws_k = __shfl_sync(0xffffffffu, wstart, (t + k) & 31);
-                if (t + k < tiles && ws_k <= w) t += k;
+                if (k < tiles) {  // warp-uniform: steps that cannot move stay out (one tile: no search)
+                    const uint32_t ws_k = __shfl_sync(0xffffffffu, wstart, (t + k) & 31);
+                    if (t + k < tiles && ws_k <= w) t += k;
+                }
             }
             const uint32_t ws_t = __shfl_sync(0xffffffffu, wstart, t);
             const uint32_t a_t = __shfl_sync(0xffffffffu, a, t);
