@@ -456,7 +456,10 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
     if (!compact_uses_counts(g) || cnt == nullptr || plist == nullptr || prow == nullptr)
         return cudaErrorNotSupported;
     const int TYT = (int)(g.ty * g.T);
-    const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(n < 65535 ? n : 65535));
+    // images in the grid's y dimension (the kernel loops over the rest); under the device-side gate
+    // (forward_auto) a quarter as many CTAs, so a skipped launch is cheap
+    const int64_t ymax = gate.flag ? 32 : 65535;
+    const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(n < ymax ? n : ymax));
     // the smallest instantiated slot count covering the plane (loads of 32 elements)
     const int64_t slots = (g.H * g.W + 31) / 32;
 #define SC_COUNT(NS)                                                                                             \
