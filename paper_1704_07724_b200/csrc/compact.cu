@@ -233,7 +233,7 @@ constexpr int kPlaneWarps = 8;
 constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 }  // namespace
 
-template <int NSLOT>
+template <int NSLOT, int IMG>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const float* __restrict__ in, int nimg, int C, int H, int W, int TYT, int P, int NWR, int tiles,
     uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow, Gate gate) {
@@ -242,16 +242,26 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     // grid (channel blocks, images): no division to split a plane index
     const int c = blockIdx.x * kPlaneWarps + warp;
     if (c >= C) return;
-    for (int n = blockIdx.y; n < nimg; n += gridDim.y) {
-    const int plane = n * C + c;
     const int HW = H * W;
-    const float* src = in + (int64_t)plane * HW;
-    float v[NSLOT];
+    // IMG images per iteration: the loads of all of them are issued first (small planes: more
+    // bytes in flight per warp)
+    for (int n0 = blockIdx.y * IMG; n0 < nimg; n0 += gridDim.y * IMG) {
+    float vv[IMG][NSLOT];
 #pragma unroll
-    for (int u = 0; u < NSLOT; ++u) {
-        const int e = 32 * u + lane;
-        v[u] = e < HW ? __ldg(src + e) : 0.0f;
+    for (int i = 0; i < IMG; ++i) {
+        const float* src = in + (int64_t)((n0 + i) * C + c) * HW;
+#pragma unroll
+        for (int u = 0; u < NSLOT; ++u) {
+            const int e = 32 * u + lane;
+            vv[i][u] = (e < HW && n0 + i < nimg) ? __ldg(src + e) : 0.0f;
+        }
     }
+#pragma unroll
+    for (int i = 0; i < IMG; ++i) {
+    const int n = n0 + i;
+    if (n >= nimg) break;
+    const int plane = n * C + c;
+    float (&v)[NSLOT] = vv[i];
     const unsigned lt = (1u << lane) - 1u;
     uint2* lst = plist + (int64_t)plane * HW;
     unsigned bal[NSLOT];
@@ -289,6 +299,7 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
     const uint32_t p0 = __shfl_sync(0xffffffffu, pre, r0), p1 = __shfl_sync(0xffffffffu, pre, r1);
     if (lane < tiles) cnt[((int64_t)n * tiles + lane) * C + c] = r1 > r0 ? p1 - p0 : 0u;
+    }
     }
 }
 
@@ -459,11 +470,14 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
     // images in the grid's y dimension (the kernel loops over the rest); under the device-side gate
     // (forward_auto) a quarter as many CTAs, so a skipped launch is cheap
     const int64_t ymax = gate.flag ? 32 : 65535;
-    const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(n < ymax ? n : ymax));
+    const int64_t slots0 = (g.H * g.W + 31) / 32;
+    const int img = slots0 <= 2 ? 2 : 1;  // planes of <= 64 elements: two images per warp iteration
+    const int64_t ny = (n + img - 1) / img;
+    const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(ny < ymax ? ny : ymax));
     // the smallest instantiated slot count covering the plane (loads of 32 elements)
     const int64_t slots = (g.H * g.W + 31) / 32;
 #define SC_COUNT(NS)                                                                                             \
-    compact_plane_count_kernel<NS><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, (int)n, (int)g.C, (int)g.H, (int)g.W,  \
+    compact_plane_count_kernel<NS, (NS <= 2 ? 2 : 1)><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, (int)n, (int)g.C, (int)g.H, (int)g.W,  \
                                                                        TYT, (int)g.P, (int)g.nwr, (int)g.tiles,   \
                                                                        cnt, plist, prow, gate)
     if (slots <= 2) SC_COUNT(2);
