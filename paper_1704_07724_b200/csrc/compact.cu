@@ -471,13 +471,13 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
     // (forward_auto) a quarter as many CTAs, so a skipped launch is cheap
     const int64_t ymax = gate.flag ? 32 : 65535;
     const int64_t slots0 = (g.H * g.W + 31) / 32;
-    const int img = slots0 <= 2 ? 2 : 1;  // planes of <= 64 elements: two images per warp iteration
+    const int img = slots0 <= 8 ? 2 : 1;  // planes of <= 256 elements: two images per warp iteration
     const int64_t ny = (n + img - 1) / img;
     const dim3 cgrid((unsigned)((g.C + kPlaneWarps - 1) / kPlaneWarps), (unsigned)(ny < ymax ? ny : ymax));
     // the smallest instantiated slot count covering the plane (loads of 32 elements)
     const int64_t slots = (g.H * g.W + 31) / 32;
 #define SC_COUNT(NS)                                                                                             \
-    compact_plane_count_kernel<NS, (NS <= 2 ? 2 : 1)><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, (int)n, (int)g.C, (int)g.H, (int)g.W,  \
+    compact_plane_count_kernel<NS, (NS <= 8 ? 2 : 1)><<<cgrid, kPlaneWarps * 32, 0, st>>>(in, (int)n, (int)g.C, (int)g.H, (int)g.W,  \
                                                                        TYT, (int)g.P, (int)g.nwr, (int)g.tiles,   \
                                                                        cnt, plist, prow, gate)
     if (slots <= 2) SC_COUNT(2);
