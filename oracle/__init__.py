@@ -6,7 +6,10 @@ computes.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 with the CUDA path (``paper_1704_07724_b200``) and never imports it.
 
 Every function cites the passage of /root/reference/PAPER.md ("P:<line>") it
-follows; readings of garbled or silent passages are DESIGN.md R1..R18.
+follows; readings of garbled or silent passages are DESIGN.md R1..R20.
+The stage-2 kernel's instruction-stream format (R9) is NOT computed here: it
+is an implementation detail of the CUDA path, derived from compact_lists by
+the test-side adapter tests/r9_adapter.py.
 
 Functions
 ---------
@@ -15,9 +18,10 @@ conv_fp64           P:68-72 (Eq. 1) + stride/pad + batch/bias/groups
                     (R2-R4); fp64 accumulation, also returns the mass
                     sum |in|*|W| that scales the parity tolerance.  (C, OpenMP)
 relu                P:74-78 (Eq. 2)
-stream_format       R9: tiles, window rows, window size, stream capacity
-compact_streams     P:123 (Sec. 4, ISC step 1) in the R9 tile-stream format (C)
-decompress_streams  inverse of compact_streams (for round-trip pins)
+list_rows           SURVEY 8c item 9: rows per list (whole plane if H*W <= 256)
+compact_lists       P:123 (Sec. 4, ISC step 1): per (image, channel, row tile)
+                    the nonzero values with their row and column, row-major (C)
+decompress_lists    inverse of compact_lists (for round-trip pins)
 dense_macs          P:109 (Sec. 4): H_out*W_out*R*S*K*C per image (with groups:
                     C/G per output channel)
 exact_nonzero_macs  P:121 (Sec. 4) "MACs can be reduce to rho*...": the exact
@@ -67,8 +71,8 @@ def _load():
         lib.oracle_conv_fp64.argtypes = [vp, vp, vp] + [i64] * 10 + [vp, vp]
         lib.oracle_conv_backward_fp64.restype = ctypes.c_int
         lib.oracle_conv_backward_fp64.argtypes = [vp, vp, vp] + [i64] * 10 + [vp] * 5
-        lib.oracle_compact_streams.restype = ctypes.c_int
-        lib.oracle_compact_streams.argtypes = [vp] + [i64] * 10 + [vp, vp]
+        lib.oracle_compact_lists.restype = ctypes.c_int
+        lib.oracle_compact_lists.argtypes = [vp] + [i64] * 5 + [vp] * 4
         _lib = lib
     return _lib
 
@@ -198,63 +202,56 @@ def conv_backward_fp64(x, w, dout, stride=1, pad=0, groups=1, want_mass=True):
 
 
 # --------------------------------------------------------------------------
-# ISC step 1: nonzero compaction in the R9 tile-stream format
+# ISC step 1: nonzero compaction as the paper states it
 # --------------------------------------------------------------------------
-def stream_format(c, h, w, r, stride, pad, ty, ho):
-    """DESIGN.md R9.  Row-tile t covers output rows [t*TY, (t+1)*TY); its input
-    window has NWR = (TY-1)*T + R rows starting at t*TY*T - P, all W columns;
-    NWIN = NWR*W.  Capacity of one (image, tile) stream = C markers + every
-    in-plane window position, rounded up to an even number of entries.
-    Returns (tiles, NWR, NWIN, cap)."""
-    tiles = -(-ho // ty)
-    nwr = (ty - 1) * stride + r
-    nwin = nwr * w
-    cap = c * (1 + min(nwr, h) * w)
-    cap += cap & 1
-    return tiles, nwr, nwin, cap
+def list_rows(h, w):
+    """SURVEY 8c item 9 (the north star leaves "row-tile" open): a list covers
+    TH consecutive input rows of one (image, channel) plane -- the whole plane
+    when H*W <= 256, else the most rows with TH*W <= 256, at least 1.
+    Returns (TH, tiles per plane, index bytes: 1 if TH*W <= 256 else 2)."""
+    if h < 1 or w < 1:
+        raise ValueError("extents must be >= 1")
+    th = h if h * w <= 256 else max(1, 256 // w)
+    return th, -(-h // th), 1 if th * w <= 256 else 2
 
 
-def compact_streams(x, r, stride, pad, ty):
-    """P:123 step 1.  x float32 [N][C][H][W] -> dict(entries u32 [N][tiles][cap][2],
-    offs u32 [N][tiles][C+1], tiles, nwr, nwin, cap).  Each channel with at
-    least one entry in the window gets a marker (c, NWIN + mask) with bit r of
-    mask set iff one of its entries sits at a window row wi with
-    wi - r = ty*stride, 0 <= ty < ty_tile; channels without entries get none
-    (offs[c] == offs[c+1]) (R9).  Entries
-    beyond offs[..][C] are left zero here and are never compared."""
+def compact_lists(x, th=None):
+    """P:123 step 1: "skip all the zero elements of the input data, and store
+    the non-zero values in a vector with their column and row information".
+
+    x float32 [N][C][H][W].  One list per (n, c, row tile t) of TH rows
+    (default: list_rows(H, W)); entries in row-major scan order, zero test
+    x != 0.0f (R7).  Returns dict(values u32, rows i32, cols i32 each
+    [N][C][tiles][TH*W] (slots at or beyond the count are zero and never
+    compared), counts u32 [N][C][tiles], th, tiles).  (C, oracle.c)"""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n, c, h, w = x.shape
-    ho = (h + 2 * pad - r) // stride + 1
-    tiles, nwr, nwin, cap = stream_format(c, h, w, r, stride, pad, ty, ho)
-    entries = np.zeros((n, tiles, cap, 2), dtype=np.uint32)
-    offs = np.zeros((n, tiles, c + 1), dtype=np.uint32)
-    rc = _load().oracle_compact_streams(_ptr(x), n, c, h, w, ty, tiles, r, stride, pad, cap,
-                                        _ptr(entries), _ptr(offs))
+    if th is None:
+        th = list_rows(h, w)[0]
+    if th < 1:
+        raise ValueError("th must be >= 1")
+    tiles = -(-h // th)
+    values = np.zeros((n, c, tiles, th * w), np.uint32)
+    rows = np.zeros((n, c, tiles, th * w), np.int32)
+    cols = np.zeros((n, c, tiles, th * w), np.int32)
+    counts = np.zeros((n, c, tiles), np.uint32)
+    rc = _load().oracle_compact_lists(_ptr(x), n, c, h, w, th, _ptr(values), _ptr(rows), _ptr(cols), _ptr(counts))
     if rc != 0:
-        raise ValueError("oracle_compact_streams: invalid arguments")
-    return dict(entries=entries, offs=offs, tiles=tiles, nwr=nwr, nwin=nwin, cap=cap, ty=ty)
+        raise ValueError("oracle_compact_lists: invalid arguments")
+    return dict(values=values, rows=rows, cols=cols, counts=counts, th=th, tiles=tiles)
 
 
-def decompress_streams(st, shape, stride, pad):
-    """Inverse of compact_streams: scatter every stream's entries back into a
-    zero tensor (inputs in several windows are written more than once, with
-    the same bits).  Also checks the markers."""
+def decompress_lists(lists, shape):
+    """Inverse of compact_lists: scatter every list's (row, col, value) back
+    into a zero tensor of `shape` (used by the round-trip pins)."""
     n, c, h, w = shape
-    out = np.zeros(shape, dtype=np.float32).reshape(n, c, h * w).view(np.uint32)
-    for ni in range(n):
-        for t in range(st["tiles"]):
-            i_lo = t * st["ty"] * stride - pad
-            e = st["entries"][ni, t]
-            of = st["offs"][ni, t]
-            for ci in range(c):
-                a, b = int(of[ci]), int(of[ci + 1])
-                if a == b:
-                    continue  # no entry in this window: no marker (R9)
-                assert b > a + 1 and e[a, 0] == ci and e[a, 1] >= st["nwin"], "bad channel marker"
-                code = e[a + 1:b, 1].astype(np.int64)
-                rows = i_lo + code // w
-                out[ni, ci, rows * w + code % w] = e[a + 1:b, 0]
-    return out.view(np.float32).reshape(shape)
+    out = np.zeros(shape, np.float32).view(np.uint32)
+    cnt = lists["counts"].astype(np.int64)
+    k = np.arange(lists["values"].shape[-1])
+    live = k[None, None, None, :] < cnt[..., None]
+    ni, ci, _, ki = np.nonzero(live)
+    out[ni, ci, lists["rows"][live], lists["cols"][live]] = lists["values"][live]
+    return out.view(np.float32)
 
 
 def tolerance_sparse(mass):

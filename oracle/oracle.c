@@ -17,10 +17,14 @@
  *                        Accumulates in double, loop order n,k,y,x | c,r,t.
  *                        Also returns mass = sum |in|*|W| over the receptive
  *                        field (the tolerance scale of the north star).
- *   oracle_compact_streams -- ISC step 1, PAPER.md:123 (Sec. 4): "skip all the
+ *   oracle_compact_lists -- ISC step 1, PAPER.md:123 (Sec. 4): "skip all the
  *                        zero elements of the input data, and store the
  *                        non-zero values in a vector with their column and row
- *                        information", in the tile-stream format of DESIGN.md R9.
+ *                        information": per (image, channel, row tile) the
+ *                        nonzero values with their (row, column), row-major.
+ *                        The kernel's own stream format (stage-2 instruction
+ *                        stream, R9) is derived from these lists by
+ *                        a test-side adapter (tests/r9_adapter.py), not here.
  *   oracle_conv_backward_fp64 -- SURVEY 8f row f4: the gradients of Eq. 1
  *                        (chain rule) for training, where the paper measures
  *                        the sparsity (Sec. 1; Sec. 3);
@@ -99,75 +103,50 @@ int oracle_conv_fp64(const float *in, const float *w, const float *bias,
 }
 
 /*
- * ISC step 1 in the tile-stream format of DESIGN.md R9:
- * "store the non-zero values in a vector with their column and row
- * information", one vector per (image n, output row-tile t).
+ * ISC step 1, PAPER.md:123 (Sec. 4, "Inverse Sparse Convolution"): "we skip all
+ * the zero elements of the input data, and store the non-zero values in a
+ * vector with their column and row information".
  *
- * Tile t covers output rows [t*TY, (t+1)*TY); its input window is rows
- * i_lo = t*TY*T - P .. i_lo + NWR - 1 with NWR = (TY-1)*T + R, all W columns,
- * NWIN = NWR*W window positions.  stream[n][t] is a sequence of 8-byte
- * entries (a, b) (u32 pairs):
- *   for c = 0..C-1 (ascending) with at least one entry in the window:
- *     marker  (a = c, b = NWIN + mask), bit r of mask set iff some entry
- *             below lies at a window row wi with wi - r = ty*T for a tile
- *             row 0 <= ty < TY (the filter rows r the channel reaches)
- *     for every input x = in[n,c,i,j] != 0.0f (IEEE compare: -0.0 is zero;
- *     subnormal/NaN/Inf are nonzero) with i inside the window and the plane,
- *     ascending (i, j):  (a = bit copy of x, b = (i - i_lo)*W + j)
- *   offs[n][t][c] = index of channel c's marker (channels without entries
- *   have none: offs[n][t][c] == offs[n][t][c+1]), offs[n][t][C] = length.
- * entries: u32 [N][tiles][cap][2]; offs: u32 [N][tiles][C+1].  Entries beyond
- * the length are not written.  Returns 0, or -1 on invalid arguments / overflow.
+ * One vector (list) per (image n, channel c, row tile t), the tile being input
+ * rows [t*TH, min((t+1)*TH, H)) of the plane (TH = H gives one
+ * list per plane).  A plain row-major scan of the plane: for every element
+ * x = in[n,c,i,j] with x != 0.0f (IEEE compare: -0.0 is zero; subnormals, NaN
+ * and Inf are nonzero -- DESIGN.md R7), in ascending (i, j):
+ *     values[l][k] = bit copy of x,  rows[l][k] = i,  cols[l][k] = j
+ * and counts[l] = number of such elements, l = (n*C + c)*tiles + t.  Every list
+ * has TH*W slots; slots at or beyond counts[l] are not written.
+ * values: u32 [N][C][tiles][TH*W]; rows, cols: i32 same; counts: u32 [N][C][tiles].
+ * Returns 0, or -1 on invalid arguments.
  */
-int oracle_compact_streams(const float *in, int64_t N, int64_t C, int64_t H, int64_t W,
-                           int64_t TY, int64_t tiles, int64_t R, int64_t T, int64_t P,
-                           int64_t cap, uint32_t *entries, uint32_t *offs)
+int oracle_compact_lists(const float *in, int64_t N, int64_t C, int64_t H, int64_t W, int64_t TH,
+                         uint32_t *values, int32_t *rows, int32_t *cols, uint32_t *counts)
 {
-    if (N < 1 || C < 1 || H < 1 || W < 1 || TY < 1 || tiles < 1 || R < 1 || T < 1 || P < 0) return -1;
-    const int64_t NWR = (TY - 1) * T + R, NWIN = NWR * W;
-    int bad = 0;
-    #pragma omp parallel for collapse(2) schedule(static) reduction(|:bad)
+    if (N < 1 || C < 1 || H < 1 || W < 1 || TH < 1) return -1;
+    const int64_t tiles = (H + TH - 1) / TH, slots = TH * W;
+    #pragma omp parallel for collapse(2) schedule(static)
     for (int64_t n = 0; n < N; ++n) {
-        for (int64_t t = 0; t < tiles; ++t) {
-            const int64_t i_lo = t * TY * T - P;
-            uint32_t *st = entries + (n * tiles + t) * cap * 2;
-            uint32_t *of = offs + (n * tiles + t) * (C + 1);
-            int64_t len = 0;
-            for (int64_t c = 0; c < C; ++c) {
-                of[c] = (uint32_t)len;
-                if (len >= cap) { bad = 1; break; }
-                const int64_t marker = len;
-                uint32_t mask = 0;  /* tap rows r reached by this channel's entries */
-                st[2 * len] = (uint32_t)c;
-                ++len;
-                for (int64_t wi = 0; wi < NWR; ++wi) {
-                    const int64_t i = i_lo + wi;
-                    if (i < 0 || i >= H) continue;
+        for (int64_t c = 0; c < C; ++c) {
+            for (int64_t t = 0; t < tiles; ++t) {
+                const int64_t l = (n * C + c) * tiles + t;
+                uint32_t k = 0;
+                for (int64_t i = t * TH; i < (t + 1) * TH && i < H; ++i) {
                     for (int64_t j = 0; j < W; ++j) {
                         const float x = in[((n * C + c) * H + i) * W + j];
                         if (x != 0.0f) {
-                            if (len >= cap) { bad = 1; break; }
                             uint32_t bits;
                             memcpy(&bits, &x, sizeof bits);
-                            st[2 * len] = bits;
-                            st[2 * len + 1] = (uint32_t)(wi * W + j);
-                            ++len;
-                            for (int64_t r = 0; r < R && r < 32; ++r) {
-                                const int64_t d = wi - r;  /* = ty*T for tile row ty */
-                                if (d >= 0 && d % T == 0 && d / T < TY) mask |= 1u << r;
-                            }
+                            values[l * slots + k] = bits;
+                            rows[l * slots + k] = (int32_t)i;
+                            cols[l * slots + k] = (int32_t)j;
+                            ++k;
                         }
                     }
                 }
-                if (len == marker + 1)
-                    len = marker;  /* no entry in this window: no marker (R9) */
-                else
-                    st[2 * marker + 1] = (uint32_t)NWIN + mask;
+                counts[l] = k;
             }
-            of[C] = (uint32_t)len;
         }
     }
-    return bad ? -1 : 0;
+    return 0;
 }
 
 /*

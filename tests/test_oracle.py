@@ -110,14 +110,12 @@ def test_hand_worked_example():
     assert np.array_equal(out.reshape(-1), np.array(g["output"], dtype=np.float64))
     assert oracle.exact_nonzero_macs(x, 1, 3, 3, 1, 1) == int(g["exact_macs"][0])
     assert oracle.dense_macs(1, 1, 3, 3, 1, 3, 3, 1, 1) == int(g["dense_macs"][0])
-    st = oracle.compact_streams(x, 3, 1, 1, 3)
-    assert st["tiles"] == 1 and st["nwin"] == 15
-    offs = st["offs"][0, 0]
-    assert list(offs) == [int(v) for v in g["stream_offs"]]
-    e = st["entries"][0, 0, :3]
-    a = [int(g["stream_a"][0])] + [int(np.float32(v).view(np.uint32)) for v in g["stream_a"][1:]]
-    assert list(e[:, 0]) == a
-    assert list(e[:, 1]) == [int(v) for v in g["stream_b"]]
+    # ISC step 1: the nonzero values with their row and column, row-major
+    lst = oracle.compact_lists(x)
+    assert lst["th"] == 3 and lst["tiles"] == 1 and int(lst["counts"][0, 0, 0]) == 2
+    assert list(lst["values"][0, 0, 0, :2]) == [int(np.float32(v).view(np.uint32)) for v in g["list_values"]]
+    assert list(lst["rows"][0, 0, 0, :2]) == [int(v) for v in g["list_rows"]]
+    assert list(lst["cols"][0, 0, 0, :2]) == [int(v) for v in g["list_cols"]]
 
 
 def _torch_ref(x, w, b, stride, pad, groups):
@@ -272,80 +270,45 @@ def test_mac_conservation_at_zero_sparsity(table2):
 
 
 # ---------------------------------------------------------------------------
-# compaction (ISC step 1) in the tile-stream format
+# compaction (ISC step 1): per (image, channel, row tile) nonzero values
+# with their row and column
 # ---------------------------------------------------------------------------
-def test_stream_format():
-    # (c, h, w, r, stride, pad, ty, ho) -> (tiles, nwr, nwin, cap)
-    assert oracle.stream_format(256, 13, 13, 3, 1, 1, 13, 13) == (1, 15, 195, 256 * (1 + 13 * 13))
-    assert oracle.stream_format(256, 13, 13, 3, 1, 1, 7, 13) == (2, 9, 117, 256 * (1 + 9 * 13))
-    assert oracle.stream_format(20, 11, 11, 5, 2, 1, 5, 5) == (1, 13, 143, 20 * (1 + 11 * 11))
-    assert oracle.stream_format(3, 5, 5, 1, 1, 0, 2, 5) == (3, 2, 10, 3 * 11 + 1)
+def test_list_rows_rule():
+    """whole plane when H*W <= 256, else TH*W <= 256 (>= 1 row)."""
+    assert oracle.list_rows(13, 13) == (13, 1, 1)      # 169 elements: one list per plane
+    assert oracle.list_rows(12, 12) == (12, 1, 1)
+    assert oracle.list_rows(16, 16) == (16, 1, 1)      # exactly 256
+    assert oracle.list_rows(28, 28) == (9, 4, 1)       # 9*28 = 252
+    assert oracle.list_rows(27, 27) == (9, 3, 1)       # 9*27 = 243
+    assert oracle.list_rows(4, 300) == (1, 4, 2)       # one row is wider than 256: u16 index
 
 
-def _window_entries_reference(x, r, stride, pad, ty):
-    """Independent construction with numpy (np.nonzero) of what every stream
-    must contain: per (n, tile, c) the ascending nonzeros inside the window."""
-    n, c, h, w = x.shape
-    ho = (h + 2 * pad - r) // stride + 1
-    tiles = -(-ho // ty)
-    nwr = (ty - 1) * stride + r
-    out = {}
-    for ni in range(n):
-        for t in range(tiles):
-            i_lo = t * ty * stride - pad
-            rows = [i for i in range(i_lo, i_lo + nwr) if 0 <= i < h]
-            for ci in range(c):
-                if rows:
-                    sub = x[ni, ci, rows[0]:rows[-1] + 1]
-                    ii, jj = np.nonzero(sub)          # row-major ascending
-                    vals = sub[ii, jj].view(np.uint32)
-                    codes = (ii + rows[0] - i_lo) * w + jj
-                else:
-                    vals = codes = np.zeros(0, np.int64)
-                out[(ni, t, ci)] = (vals.astype(np.uint32), codes.astype(np.uint32))
-    return out, tiles, nwr * w
-
-
-@pytest.mark.parametrize("shape,r,stride,pad,ty", [((2, 3, 13, 13), 3, 1, 1, 13), ((2, 3, 13, 13), 3, 1, 1, 7),
-                                                  ((1, 2, 28, 28), 3, 1, 1, 3), ((2, 2, 27, 27), 5, 1, 2, 2),
-                                                  ((1, 4, 11, 11), 5, 2, 1, 5), ((2, 3, 7, 7), 1, 1, 0, 3),
-                                                  ((3, 2, 1, 1), 1, 1, 0, 1)])
-def test_compact_streams_against_numpy_and_roundtrip(shape, r, stride, pad, ty):
-    rng = np.random.default_rng(sum(shape) + ty)
+@pytest.mark.parametrize("shape,th", [((2, 3, 13, 13), None), ((2, 3, 13, 13), 4), ((1, 2, 28, 28), None),
+                                      ((2, 2, 27, 27), 1), ((3, 2, 1, 1), None), ((1, 1, 5, 300), None)])
+def test_compact_lists_against_numpy_and_roundtrip(shape, th):
+    """Each list = np.nonzero of its rows (row-major), values as bit copies; the
+    decompressed lists give back the input bit for bit."""
+    rng = np.random.default_rng(sum(shape))
     x = (np.abs(rng.standard_normal(shape)) * (rng.random(shape) > 0.85)).astype(np.float32)
-    st = oracle.compact_streams(x, r, stride, pad, ty)
-    ref, tiles, nwin = _window_entries_reference(x, r, stride, pad, ty)
-    assert st["tiles"] == tiles and st["nwin"] == nwin
-    n, c = shape[:2]
+    lst = oracle.compact_lists(x, th)
+    n, c, h, w = shape
+    th = lst["th"]
+    assert lst["tiles"] == -(-h // th)
     for ni in range(n):
-        for t in range(tiles):
-            of = st["offs"][ni, t].astype(np.int64)
-            e = st["entries"][ni, t]
-            for ci in range(c):
-                a, b = of[ci], of[ci + 1]
-                vals, codes = ref[(ni, t, ci)]
-                # marker mask: filter rows r reached by some entry (window row wi = r + ty*stride)
-                mask = 0
-                for wi in set((codes // shape[3]).tolist()):
-                    for rr in range(r):
-                        d = wi - rr
-                        if d >= 0 and d % stride == 0 and d // stride < ty:
-                            mask |= 1 << rr
-                if len(vals) == 0:
-                    assert a == b  # no entry in the window: no marker (R9)
-                    continue
-                assert e[a, 0] == ci and e[a, 1] == nwin + mask
-                assert np.array_equal(e[a + 1:b, 0], vals)
-                assert np.array_equal(e[a + 1:b, 1], codes)
-    back = oracle.decompress_streams(st, shape, stride, pad)
-    covered = np.zeros(shape[2], bool)
-    for t in range(tiles):
-        lo = t * ty * stride - pad
-        covered[max(lo, 0):max(min(lo + (ty - 1) * stride + r, shape[2]), 0)] = True
-    assert np.array_equal(back[:, :, covered].view(np.uint32), x[:, :, covered].view(np.uint32))
+        for ci in range(c):
+            for t in range(lst["tiles"]):
+                sub = x[ni, ci, t * th:(t + 1) * th]
+                ii, jj = np.nonzero(sub)
+                k = int(lst["counts"][ni, ci, t])
+                assert k == len(ii) == np.count_nonzero(sub)
+                assert np.array_equal(lst["values"][ni, ci, t, :k], sub[ii, jj].view(np.uint32))
+                assert np.array_equal(lst["rows"][ni, ci, t, :k], ii + t * th)
+                assert np.array_equal(lst["cols"][ni, ci, t, :k], jj)
+    back = oracle.decompress_lists(lst, shape)
+    assert np.array_equal(back.view(np.uint32), x.view(np.uint32))
 
 
-def test_compact_streams_zero_semantics():
+def test_compact_lists_zero_semantics():
     """R7: IEEE compare x != 0.0f: -0.0 is zero; subnormals, NaN, Inf are not."""
     x = np.zeros((1, 1, 2, 4), np.float32)
     x[0, 0, 0, 0] = -0.0
@@ -353,11 +316,29 @@ def test_compact_streams_zero_semantics():
     x[0, 0, 0, 2] = np.nan
     x[0, 0, 1, 0] = np.inf
     x[0, 0, 1, 3] = -2.5
-    st = oracle.compact_streams(x, 1, 1, 0, 2)
-    e = st["entries"][0, 0]
-    assert int(st["offs"][0, 0, 1]) == 5
-    assert list(e[1:5, 1]) == [1, 2, 4, 7]
-    assert e[1, 0] == np.float32(1e-45).view(np.uint32)
+    lst = oracle.compact_lists(x)
+    assert int(lst["counts"][0, 0, 0]) == 4
+    assert list(lst["rows"][0, 0, 0, :4]) == [0, 0, 1, 1]
+    assert list(lst["cols"][0, 0, 0, :4]) == [1, 2, 0, 3]
+    assert lst["values"][0, 0, 0, 0] == np.float32(1e-45).view(np.uint32)
+    assert lst["values"][0, 0, 0, 3] == np.float32(-2.5).view(np.uint32)
+
+
+def test_sparsity_pins():
+    """P:121: sparsity = 1 - #nonzeros/size, exact IEEE zero test (R7).
+    7 nonzeros (a subnormal, NaN, Inf and negative values among them) in 100
+    elements with a -0.0 -> 0.93; all-zero -> 1; dense -> 0."""
+    x = np.zeros(100, np.float32)
+    x[3] = -0.0
+    x[[5, 17, 40]] = [1.0, -3.0, 0.5]
+    x[50] = np.float32(1e-45)
+    x[60] = np.nan
+    x[70] = -np.inf
+    x[99] = 2.0
+    assert oracle.sparsity(x) == pytest.approx(0.93, abs=1e-15)
+    assert oracle.sparsity(np.zeros((4, 5), np.float32)) == 1.0
+    assert oracle.sparsity(np.ones((3, 3), np.float32)) == 0.0
+    assert oracle.sparsity(-np.zeros(8, np.float32)) == 1.0
 
 
 # ---------------------------------------------------------------------------
@@ -401,20 +382,3 @@ def test_relu_of_symmetric_tensor_half_sparse():
     assert abs(oracle.sparsity(z) - 0.5) <= 0.02
     assert np.array_equal(oracle.relu(z), z)
     assert np.all(z >= 0)
-
-
-def test_compact_streams_empty_channels_have_no_marker():
-    """R9: a channel with no nonzero inside a tile's window contributes nothing to that
-    tile's stream (offs[c] == offs[c+1]); the others keep marker + entries in order."""
-    x = np.zeros((1, 3, 6, 4), np.float32)
-    x[0, 0, 0, 1] = 1.0      # only in tile 0's window (rows -1..2 with ty=2, r=3, pad=1)
-    x[0, 2, 5, 2] = 2.0      # only in the last tile's window
-    st = oracle.compact_streams(x, 3, 1, 1, 2)
-    assert st["tiles"] == 3
-    of = st["offs"][0].astype(np.int64)
-    e = st["entries"][0]
-    assert list(of[0]) == [0, 2, 2, 2]             # tile 0: channel 0 only
-    assert e[0, 0, 0] == 0 and e[0, 1, 1] == 1 * 4 + 1
-    assert list(of[1]) == [0, 0, 0, 0]             # tile 1 (rows 1..4): empty stream
-    assert list(of[2]) == [0, 0, 0, 2]             # tile 2 (rows 3..6): channel 2 only
-    assert e[2, 0, 0] == 2 and e[2, 1, 1] == (5 - 3) * 4 + 2
