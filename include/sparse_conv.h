@@ -241,6 +241,33 @@ sc_status sparse_conv_gather(sc_plan plan, int64_t n, float *d_out, sc_stream_t 
 /* Describe the plan's list workspace (device pointers, layout). */
 sc_status sparse_conv_lists(sc_plan plan, sc_lists_view *out);
 
+/* The paper-level stage-1 lists (ISC step 1, Sec. 4: "store the
+ * non-zero values in a vector with their column and row information") as the
+ * plan's plane-major compaction builds them, before it regroups them into the
+ * stage-2 streams above.  Plane p = n*C + c; entries are u32 pairs
+ * (bit copy of x, flat position i*W + j) of every x = in[n,c,i,j] != 0.0f
+ * (R7), in row-major order.
+ *   layout 1 (stage 1 read an input tensor): entries[p*H*W + k] for
+ *     k < row_counts[p*(H+1) + H]; row_counts[p*(H+1) + i] = nonzeros of the
+ *     plane before row i (exclusive row prefix), so row i's entries are
+ *     k in [row_counts[p*(H+1)+i], row_counts[p*(H+1)+i+1]).
+ *   layout 2 (chained layer, sparse_conv_forward_chain: written by the
+ *     producing layer's epilogue): one slot per row,
+ *     entries[(p*H + i)*W + k] for k < row_counts[p*H + i].
+ * Device pointers owned by the plan, valid until its next call; read them after
+ * synchronizing the stream of the call that produced them.  SC_ERR_UNSUPPORTED
+ * when the last stage 1 of the plan kept no plane lists (planes of more than
+ * 1024 elements or 31 rows use the streamwise compaction; sparse_conv_forward_auto
+ * may skip stage 1; no compaction has run yet). */
+typedef struct {
+    const uint32_t *entries;
+    const uint32_t *row_counts;
+    int64_t planes;            /* N*C of the plan (params.n images) */
+    int32_t height, width;     /* H, W of the input planes */
+    int32_t layout;            /* 1 or 2, see above */
+} sc_plane_lists_view;
+sc_status sparse_conv_plane_lists(sc_plan plan, sc_plane_lists_view *out);
+
 /* Which stage-2 kernel this plan launches: 0 = generic gather kernel (any
  * stride/shape), >0 = a shape-specialised register-tile kernel variant id. */
 sc_status sparse_conv_kernel_variant(sc_plan plan, int32_t *variant, const char **name);

@@ -32,6 +32,9 @@ struct sc_plan_s {
     uint32_t* cnt = nullptr;   // stage-1 counts [N][tiles][C] (plane-major compaction)
     uint2* plist = nullptr;    // stage-1 per-plane compacted lists [N*C][H*W]
     uint32_t* prow = nullptr;  // stage-1 per-plane row prefixes [N*C][H+1]
+    // what plist/prow hold after the last enqueued stage 1 (sparse_conv_plane_lists):
+    // 0 nothing valid, 1 plane lists + row prefixes, 2 a producer's per-row slots + row counts
+    int lists_layout = 0;
     int variant = 0;           // > 0 generated variant, 0 generic kernel, -1 run-time generated (jit.cu)
     const char* variant_name = "generic";
     sc::jit::Params jp;        // variant -1: its parameters, kernels (ungated, gated) and shared memory
@@ -243,6 +246,7 @@ cudaError_t enqueue_sparse(sc_plan_s* p, int64_t n, const float* d_in, float* d_
     uint32_t* offs = p->offs + img0 * g.tiles * (g.C + 1);
     cudaError_t e = sc::launch_compact(g, n, d_in, cnt, plist, prow, entries, offs, s, gate);
     if (e != cudaSuccess) return e;
+    p->lists_layout = (gate.flag == nullptr && sc::compact_uses_counts(g) && cnt && plist && prow) ? 1 : 0;
     return launch_stage2(p, n, entries, offs, d_out, nullptr, nullptr, s, gate);
 }
 
@@ -447,6 +451,7 @@ sc_status sparse_conv_compact(sc_plan plan, int64_t n, const float* d_in, sc_str
     DeviceGuard guard(plan->device);
     cudaError_t e = sc::launch_compact(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, plan->entries,
                                        plan->offs, (cudaStream_t)stream);
+    plan->lists_layout = (e == cudaSuccess && sc::compact_uses_counts(plan->g) && plan->plist && plan->prow) ? 1 : 0;
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "compact launch");
 }
 
@@ -589,6 +594,7 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
             e = sc::launch_compact(p->g, n, d_outs[l - 1], p->cnt, p->plist, p->prow, p->entries, p->offs, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "chain stage 1");
+        if (!lists_ready) p->lists_layout = (sc::compact_uses_counts(p->g) && p->plist && p->prow) ? 1 : 0;
         sc_plan_s* next = l + 1 < nplans ? plans[l + 1] : nullptr;
         const bool emit = next && p->variant > 0 && sc::gather_fast_can_emit(p->variant) &&
                           sc::compact_uses_counts(next->g) && next->plist && next->prow;
@@ -597,6 +603,7 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
         e = launch_stage2(p, n, p->entries, p->offs, out, emit ? next->plist : nullptr, emit ? next->prow : nullptr,
                           s);
         if (e != cudaSuccess) return cuda_fail(e, "chain gather");
+        if (emit) next->lists_layout = 2;
         lists_ready = emit;
     }
     return SC_OK;
@@ -725,7 +732,10 @@ sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float* d_in, const
     DeviceGuard guard(plan->device);
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
-    if (d_dw || d_dz) e = sc::launch_plane_lists(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, s);
+    if (d_dw || d_dz) {
+        e = sc::launch_plane_lists(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, s);
+        plan->lists_layout = e == cudaSuccess ? 1 : 0;
+    }
     if (e == cudaSuccess)
         e = sc::launch_backward(plan->g, plan->bg, n, plan->plist, plan->prow, d_dout, plan->wpack, plan->bws, d_dw,
                                 d_dbias, d_dz, s);
@@ -743,6 +753,20 @@ sc_status sparse_conv_lists(sc_plan plan, sc_lists_view* out) {
     out->window_rows = (int32_t)plan->g.nwr;
     out->window_width = (int32_t)plan->g.W;
     out->marker_code = (int32_t)plan->g.nwin;
+    return SC_OK;
+}
+
+sc_status sparse_conv_plane_lists(sc_plan plan, sc_plane_lists_view* out) {
+    if (!plan || !out) return fail(SC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (plan->lists_layout == 0 || !plan->plist || !plan->prow)
+        return fail(SC_ERR_UNSUPPORTED, "no plane lists: the plan's last stage 1 kept none (streamwise path, "
+                                        "device-side path selection, or no compaction yet)");
+    out->entries = reinterpret_cast<const uint32_t*>(plan->plist);
+    out->row_counts = plan->prow;
+    out->planes = plan->g.N * plan->g.C;
+    out->height = (int32_t)plan->g.H;
+    out->width = (int32_t)plan->g.W;
+    out->layout = plan->lists_layout;
     return SC_OK;
 }
 

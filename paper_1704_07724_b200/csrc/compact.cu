@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
             en0[q] = make_uint2(0u, 0u);
         } else {
             pv[q] = (ch < nch && lane <= H) ? __ldg(prow + (int64_t)plane * (H + 1) + lane) : 0u;
-            en0[q] = ch < nch ? __ldg(plist + (int64_t)plane * HW + lane) : make_uint2(0u, 0u);
+            // lanes past a small plane (HW < 32) load nothing: the last plane ends the allocation
+            en0[q] = (ch < nch && lane < HW) ? __ldg(plist + (int64_t)plane * HW + lane) : make_uint2(0u, 0u);
         }
     }
     // ---- stream offsets of this chunk's channels in every tile stream

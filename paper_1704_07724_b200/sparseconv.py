@@ -25,7 +25,7 @@ EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forwar
            "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
            "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
            "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward", "sc_jit_variant_source",
-           "sc_jit_available")
+           "sc_jit_available", "sparse_conv_plane_lists")
 SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
@@ -44,6 +44,11 @@ class ListsView(ctypes.Structure):
     _fields_ = [("entries", ctypes.c_void_p), ("offsets", ctypes.c_void_p), ("tiles_per_image", ctypes.c_int64),
                 ("stream_capacity", ctypes.c_int64), ("channels", ctypes.c_int64), ("tile_rows", ctypes.c_int32),
                 ("window_rows", ctypes.c_int32), ("window_width", ctypes.c_int32), ("marker_code", ctypes.c_int32)]
+
+
+class PlaneListsView(ctypes.Structure):
+    _fields_ = [("entries", ctypes.c_void_p), ("row_counts", ctypes.c_void_p), ("planes", ctypes.c_int64),
+                ("height", ctypes.c_int32), ("width", ctypes.c_int32), ("layout", ctypes.c_int32)]
 
 
 _lib = None
@@ -259,6 +264,25 @@ class SparseConv:
             offs = torch.as_tensor(_DevArray(v.offsets, (n, tiles, c + 1), "<i4"), device=self.device)
         return dict(entries=entries, offs=offs, ty=v.tile_rows, tiles=tiles, nwr=v.window_rows,
                     nwin=v.marker_code, cap=cap)
+
+    def plane_lists(self, n):
+        """Device views (int32 bit patterns) of the paper-level stage-1 lists
+         of the first n images, as sparse_conv_plane_lists describes:
+        dict(layout, entries, row_counts, h, w).  layout 1: entries
+        [n*C][H*W][2], row_counts [n*C][H+1] (exclusive row prefix); layout 2:
+        entries [n*C][H][W][2] per-row slots, row_counts [n*C][H]."""
+        v = PlaneListsView()
+        _check(lib().sparse_conv_plane_lists(self._plan, ctypes.byref(v)))
+        planes = n * (v.planes // self.params.n)
+        h, w = v.height, v.width
+        with torch.cuda.device(self.device):
+            if v.layout == 1:
+                ent = torch.as_tensor(_DevArray(v.entries, (planes, h * w, 2), "<i4"), device=self.device)
+                rc = torch.as_tensor(_DevArray(v.row_counts, (planes, h + 1), "<i4"), device=self.device)
+            else:
+                ent = torch.as_tensor(_DevArray(v.entries, (planes, h, w, 2), "<i4"), device=self.device)
+                rc = torch.as_tensor(_DevArray(v.row_counts, (planes, h), "<i4"), device=self.device)
+        return dict(layout=v.layout, entries=ent, row_counts=rc, h=h, w=w)
 
     @property
     def variant(self):

@@ -11,6 +11,7 @@ import torch
 
 import oracle
 from paper_1704_07724_b200 import datagen
+from lists_check import check_plane_lists, check_streams
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
@@ -30,9 +31,8 @@ def run_chain(n, images):
         y = conv.forward(x)
         torch.cuda.synchronize()
         xin = x.cpu().numpy()
-        lists = conv.lists(n)
-        ref_l = oracle.compact_streams(xin, shp.r, shp.stride, shp.pad, lists["ty"])
-        assert np.array_equal(lists["offs"].cpu().numpy().view(np.uint32), ref_l["offs"]), f"layer {li} offsets"
+        assert check_plane_lists(conv, xin, n), f"layer {li}: no plane lists"
+        check_streams(conv, xin, n)
         got = y.cpu().numpy()
         for i in images:
             ref, mass = oracle.conv_fp64(xin[i:i + 1], w, b, shp.stride, shp.pad, shp.groups)
@@ -73,8 +73,8 @@ def _chain_setup(n):
 def test_chain_fused_lists_match_compaction_and_oracle(n):
     """f1: intermediate layers emit the next layer's stage-1 lists from
     their epilogue.  With the intermediate outputs also materialised, every
-    consumer's R9 streams must equal oracle.compact_streams of the producer's
-    output bit for bit, and every layer must meet the tolerance on its own
+    consumer's paper-level lists must equal oracle.compact_lists of the
+    producer's output bit for bit (and its R9 streams the adapter's derivation), and every layer must meet the tolerance on its own
     input (R14); without them the final output must be bit-identical."""
     sc, layers, weights, convs, x = _chain_setup(n)
     outs = [torch.empty((n,) + c.out_shape, device=DEV) for c in convs]
@@ -83,15 +83,12 @@ def test_chain_fused_lists_match_compaction_and_oracle(n):
     inputs = [x] + outs[:-1]
     for li, (shp, conv) in enumerate(zip(layers, convs)):
         xin = inputs[li].cpu().numpy()
-        lists = conv.lists(n)
-        ref_l = oracle.compact_streams(xin, shp.r, shp.stride, shp.pad, lists["ty"])
-        offs = lists["offs"].cpu().numpy().view(np.uint32)
-        assert np.array_equal(offs, ref_l["offs"]), f"layer {li}: stream offsets"
-        length = ref_l["offs"][:, :, -1]
-        valid = np.arange(ref_l["cap"])[None, None, :] < length[:, :, None]
-        ge = lists["entries"].cpu().numpy().view(np.uint32)
-        assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref_l["entries"], 0)), \
-            f"layer {li}: stream entries"
+        # layer 0: lists of the input tensor (layout 1); later layers: the per-row lists the
+        # producer's epilogue emitted (layout 2) -- both against the oracle's lists of the
+        # materialised producer output
+        assert check_plane_lists(conv, xin, n), f"layer {li}: no plane lists"
+        assert conv.plane_lists(n)["layout"] == (1 if li == 0 else 2)
+        check_streams(conv, xin, n)
         w, b = weights[li]
         got = outs[li].cpu().numpy()
         for i in sorted({0, n - 1}):

@@ -4,7 +4,8 @@ no generated variant), the streamwise stage 1 (planes > 1024 elements or > 31
 rows), strides 1-3, pads 0-3, groups 1-4, rectangular kernels, filter counts
 that are not multiples of 32, one-pixel planes and outputs.
 
-Per shape: stage-1 streams bit-exact against oracle.compact_streams; sparse
+Per shape: stage-1 lists bit-exact against oracle.compact_lists (and the
+streams against the test-side adapter's derivation from them); sparse
 forward within the north-star bar 1e-5*mass + 1e-6; dense forward (where the
 shape is supported) within the TF32 bar 2^-9*mass + 1e-6; integer data
 bit-exact on both; backward (where supported) bit-exact on integer data."""
@@ -13,6 +14,7 @@ import pytest
 import torch
 
 import oracle
+from lists_check import check_plane_lists, check_streams
 from paper_1704_07724_b200 import datagen
 
 pytestmark = pytest.mark.gpu
@@ -69,14 +71,8 @@ def test_fuzz_shape(sc, shp):
     xd = torch.from_numpy(x).to(DEV)
     out = conv.forward(xd).cpu().numpy()
     # stage 1 bit-exact
-    lists = conv.lists(shp.n)
-    ref_l = oracle.compact_streams(x, shp.r, shp.stride, shp.pad, lists["ty"])
-    offs = lists["offs"].cpu().numpy().view(np.uint32)
-    assert np.array_equal(offs, ref_l["offs"])
-    length = ref_l["offs"][:, :, -1]
-    valid = np.arange(ref_l["cap"])[None, None, :] < length[:, :, None]
-    ge = lists["entries"].cpu().numpy().view(np.uint32)
-    assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref_l["entries"], 0))
+    check_plane_lists(conv, x, shp.n)
+    check_streams(conv, x, shp.n)
     # forward, sparse and dense
     ref, mass = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
     assert np.all(np.abs(out - ref) <= oracle.tolerance_sparse(mass)), conv.variant

@@ -13,6 +13,7 @@ import torch
 
 import oracle
 from paper_1704_07724_b200 import datagen
+from lists_check import check_plane_lists, check_streams
 
 pytestmark = pytest.mark.gpu
 
@@ -31,20 +32,18 @@ def make_conv(sc, shp, w, b, relu=False, max_batch=None):
                          max_batch or shp.n, shp.c, shp.h, shp.w, shp.stride, shp.pad, shp.groups, fuse_relu=relu)
 
 
-def check_lists(conv, x, n):
-    """Bit-exact comparison of the GPU stage-1 tile streams with
-    oracle.compact_streams for the plan's tile height (entries beyond each
-    stream's length are never compared)."""
-    p = conv.params
-    got = conv.lists(n)
-    ref = oracle.compact_streams(x[:n], p.r, p.stride, p.pad, got["ty"])
-    assert (got["tiles"], got["nwr"], got["nwin"], got["cap"]) == (ref["tiles"], ref["nwr"], ref["nwin"], ref["cap"])
-    offs = got["offs"].cpu().numpy().view(np.uint32)
-    assert np.array_equal(offs, ref["offs"])
-    length = ref["offs"][:, :, -1]
-    valid = np.arange(ref["cap"])[None, None, :] < length[:, :, None]
-    ge = got["entries"].cpu().numpy().view(np.uint32)
-    assert np.array_equal(np.where(valid[..., None], ge, 0), np.where(valid[..., None], ref["entries"], 0))
+# Tile height the stage-2 stream layout uses for each BASELINE config (the shipped
+# variants): stated here so a plan that silently changed its
+# layout fails the stream check instead of being compared against itself.
+EXPECTED_TY = {"C1": 6, "C2": 2, "C3": 3, "C4a": 1, "C4b": 4}
+
+
+def check_lists(conv, x, n, cfg=None):
+    """Stage 1 bit-exact: (a) the paper-level lists against
+    oracle.compact_lists; (b) the stage-2 streams against the test-side
+    adapter's derivation from the same oracle lists (tests/r9_adapter.py)."""
+    check_plane_lists(conv, x, n)
+    check_streams(conv, x, n, EXPECTED_TY.get(cfg))
 
 
 def check_conv(got, x, w, b, shp, relu=False, images=None):
@@ -80,7 +79,7 @@ def test_full_config_lists_bitexact_and_sampled_outputs(sc, cfg, s):
     xd = torch.from_numpy(x).to(DEV)
     out = conv.forward(xd)
     torch.cuda.synchronize()
-    check_lists(conv, x, shp.n)
+    check_lists(conv, x, shp.n, cfg)
     got = out.cpu().numpy()
     check_conv(got, x, w, b, shp, images=[0, 1, shp.n // 2, shp.n - 1])
 
@@ -96,7 +95,7 @@ def test_small_batch_all_outputs(sc, cfg, s):
     conv = make_conv(sc, shp, w, b, max_batch=8)
     out = conv.forward(torch.from_numpy(x).to(DEV))
     torch.cuda.synchronize()
-    check_lists(conv, x, 3)
+    check_lists(conv, x, 3, cfg)
     check_conv(out.cpu().numpy(), x, w, b, shp)
 
 
@@ -289,23 +288,38 @@ def test_c5_chain_per_layer(sc):
         xd = out
 
 
+# Every stage-2 kernel that matches a config: the generic kernel (0), the shipped variant,
+# and the superseded round-1 tilings (tools/gen_gather.py SUPERSEDED: no longer built into the
+# library), generated at run time through SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE".
+JIT_TILINGS = {1: "7,2,7,1,8,4,3,254", 2: "3,2,7,1,8,4,3,254", 3: "2,2,7,1,4,4,3,254", 4: "2,2,7,1,4,4,3,254",
+               7: "7,1,11,1,16,4,3,254", 10: "3,3,11,1,8,4,3,254", 11: "3,4,7,1,8,3,3,254",
+               12: "2,4,11,1,8,3,3,254", 13: "5,2,11,1,8,4,3,254", 14: "1,4,11,1,8,3,3,254",
+               30: "2,1,11,1,16,2,3,254"}
 FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28)] +
           [("C4b", v) for v in (0, 4, 29, 30)] + [("C3", v) for v in (0, 3, 33)])
+
+
+def force_kernel(monkeypatch, variant):
+    """Select stage-2 kernel `variant` for plans created from now on; returns the
+    variant id the plan must report (-1 for a run-time generated tiling)."""
+    if variant in JIT_TILINGS:
+        monkeypatch.setenv("SC_JIT_FORCE", JIT_TILINGS[variant])
+        return -1
+    monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
+    return variant
 
 
 @pytest.mark.parametrize("cfg,variant", FORCED)
 @pytest.mark.parametrize("s", [0.0, 0.95])
 def test_forced_variants(sc, cfg, variant, s, monkeypatch):
-    """Every stage-2 kernel that matches C2 / C4a (generic = 0, and each
-    generated register-tile variant of tools/gen_gather.py) against the
-    oracle via SC_FORCE_VARIANT: tolerance on seeded data (dense s=0 too) and
-    bit-exact on integer data."""
-    monkeypatch.setenv("SC_FORCE_VARIANT", str(variant))
+    """Every stage-2 kernel that matches C2 / C4a / C4b / C3 against the oracle:
+    tolerance on seeded data (dense s=0 too) and bit-exact on integer data."""
+    want = force_kernel(monkeypatch, variant)
     shp = datagen.CONFIGS[cfg].with_batch(5)
     x = datagen.activations(shp, "channel" if (cfg == "C3" and s > 0) else s, seed=3)
     w, b = datagen.weights(shp, seed=3)
     conv = make_conv(sc, shp, w, b, max_batch=9)
-    assert conv.variant[0] == variant
+    assert conv.variant[0] == want
     out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
     check_lists(conv, x, 5)
     check_conv(out, x, w, b, shp)
