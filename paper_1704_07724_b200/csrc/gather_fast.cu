@@ -26,7 +26,7 @@ int gather_fast_select(const Geometry& g, int force, const char** name, int* kl,
     *ty = (int)g.Ho;
     if (force == 0) return 0;
 #define SC_SELECT(VV)                                       \
-    if (matches<VV>(g) && ((force < 0 && VV::ID < 90) || force == VV::ID)) { \
+    if (matches<VV>(g) && (force < 0 || force == VV::ID)) { \
         if (name) *name = VV::NAME;                         \
         *kl = VV::KL;                                       \
         *ty = VV::TY;                                       \

@@ -38,21 +38,11 @@ OUT = os.path.join(ROOT, "paper_1704_07724_b200", "csrc", "gather_variants.inc")
 # NW compute warps (+1 producer warp) per CTA, MINB CTAs per SM (register budget
 # 65536 / (32*(NW+1)*MINB)).
 VARIANTS = [
-    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 7, 1, 8, 4),      # C2, C5 (AlexNet conv3/4/5)
-    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 7, 1, 8, 4),      # C4a (inception-3a 3x3)
-    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 7, 1, 4, 4),      # C3 (AlexNet conv2, groups 2)
-    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 7, 1, 4, 4),      # C4b (inception-3a 5x5)
     (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 (LeNet conv2)
-    (7, "r3s3p1_w13_ty7_kl1_nw11", 3, 3, 1, 13, 7, 1, 11, 1, 16, 4),  # C2: x-pairs, 3 warps/SMSP
-    (10, "r3s3p1_w13_ty3_kl3_nw11", 3, 3, 1, 13, 3, 3, 11, 1, 8, 4),  # C2: k-triples, 3 warps/SMSP
-    (11, "r3s3p1_w13_ty3_kl4_nw7", 3, 3, 1, 13, 3, 4, 7, 1, 8, 3),    # C2: k-quads, 2 warps/SMSP
-    (12, "r3s3p1_w13_ty2_kl4_nw11", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3),  # C2: k-quads, 3 warps/SMSP
-    (13, "r3s3p1_w13_ty5_kl2_nw11", 3, 3, 1, 13, 5, 2, 11, 1, 8, 4),  # C2: k-pairs, 3 warps/SMSP
-    (14, "r3s3p1_w28_ty1_kl4_nw11", 3, 3, 1, 28, 1, 4, 11, 1, 8, 3),  # C4a: k-quads
-    # V12 with 16-channel weight chunks in a 2-stage ring: half the chunk boundaries (pieces, barrier
-    # handshakes); measured best of the CH/STAGES/SLOTS/PIECE sweep
-    (21, "r3s3p1_w13_ty2_kl4_nw11_ch16s2", 3, 3, 1, 13, 2, 4, 11, 1, 16, 2),
-    (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a
+    # k-quads, 3 warps/SMSP, 16-channel weight chunks in a 2-stage ring: measured best of the
+    # CH/STAGES/SLOTS/PIECE sweep
+    (21, "r3s3p1_w13_ty2_kl4_nw11_ch16s2", 3, 3, 1, 13, 2, 4, 11, 1, 16, 2),   # C2, C5 (AlexNet conv3/4/5)
+    (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a (inception-3a 3x3)
     (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
     (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
     # paper Table 2 shapes: stride 2, 1x1, small planes
@@ -67,17 +57,32 @@ VARIANTS = [
     (45, "r1s1p0_w7_ty2_kl2_sl2", 1, 1, 0, 7, 2, 2, 11, 1, 16, 2, None, 2, 254),           # Inception5a.2
     (46, "r3s3p1_w7_ty2_kl4_p126", 3, 3, 1, 7, 2, 4, 11, 1, 16, 2, None, 3, 126),          # Inception5b.3
     (47, "r5s5p2_w7_ty2_kl2_sl2p126", 5, 5, 2, 7, 2, 2, 11, 1, 16, 2, None, 2, 126),       # Inception5b.5
-    (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),        # C4b
 ]
 
-# ablations of V12 for timing studies only (wrong results: never selected unless forced)
+# Superseded round-1 tilings (slower than the shipped variant of the same shape, DESIGN.md
+# "Stage 2") and the V12 ablations (wrong results by design: timing studies only).  Not built
+# into libsparseconv.so; any of them can be generated at run time for tuning or tests with
+# SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE" (csrc/jit.cu).
+SUPERSEDED = [
+    (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 7, 1, 8, 4),      # C2
+    (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 7, 1, 8, 4),      # C4a
+    (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 7, 1, 4, 4),      # C3
+    (4, "r5s5p2_w28_ty2_kl2", 5, 5, 2, 28, 2, 2, 7, 1, 4, 4),      # C4b
+    (7, "r3s3p1_w13_ty7_kl1_nw11", 3, 3, 1, 13, 7, 1, 11, 1, 16, 4),  # C2: x-pairs
+    (10, "r3s3p1_w13_ty3_kl3_nw11", 3, 3, 1, 13, 3, 3, 11, 1, 8, 4),  # C2: k-triples
+    (11, "r3s3p1_w13_ty3_kl4_nw7", 3, 3, 1, 13, 3, 4, 7, 1, 8, 3),    # C2: k-quads, 2 warps/SMSP
+    (12, "r3s3p1_w13_ty2_kl4_nw11", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3),  # C2: V21 with 8-channel chunks
+    (13, "r3s3p1_w13_ty5_kl2_nw11", 3, 3, 1, 13, 5, 2, 11, 1, 8, 4),  # C2: k-pairs
+    (14, "r3s3p1_w28_ty1_kl4_nw11", 3, 3, 1, 28, 1, 4, 11, 1, 8, 3),  # C4a: k-quads
+    (30, "r5s5p2_w28_ty2_kl1_nw11", 5, 5, 2, 28, 2, 1, 11, 1, 16, 2),  # C4b
+]
 ABLATIONS = [
     (90, "ablate_v12_noload", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3, "noload"),
     (91, "ablate_v12_nofma", 3, 3, 1, 13, 2, 4, 11, 1, 8, 3, "nofma"),
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 12, 11, 10, 13, 7, 1, 28, 14, 2, 29, 30, 4, 33, 3, 48, 49]  # 48/49 need Kg >= KMIN
+PRIORITY = [21, 28, 29, 33, 48, 49]  # 48/49 need Kg >= KMIN
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):
@@ -301,10 +306,10 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
 def main():
     parts = ["// GENERATED by tools/gen_gather.py -- do not edit.  See that script for the derivation.",
              "#pragma once", ""]
-    for v in VARIANTS + ABLATIONS:
+    for v in VARIANTS:
         parts.append(gen_variant(*v))
         parts.append("")
-    order = sorted(VARIANTS + ABLATIONS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
+    order = sorted(VARIANTS, key=lambda v: PRIORITY.index(v[0]) if v[0] in PRIORITY else 100 + v[0])
     parts.append("#define SC_GATHER_VARIANTS(X) \\")
     parts.append(" \\\n".join(f"    X(V{v[0]})" for v in order))
     parts.append("")
@@ -316,7 +321,7 @@ def main():
     for fn in os.listdir(csrc):
         if fn.startswith("gather_fast_v") and fn.endswith(".cu"):
             os.remove(os.path.join(csrc, fn))
-    for v in VARIANTS + ABLATIONS:
+    for v in VARIANTS:
         with open(os.path.join(csrc, f"gather_fast_v{v[0]}.cu"), "w") as f:
             f.write(f"// Variant V{v[0]} of the register-tile gather kernel (see gather_fast_impl.cuh).\n"
                     f"#include \"gather_fast_impl.cuh\"\nSC_INSTANTIATE_VARIANT(V{v[0]})\n")
