@@ -208,6 +208,15 @@ def cpu_oracle_rate(layers, x_imgs, weights, min_s=10.0, max_s=30.0):
     return flops * done / el / 1e9, done, el
 
 
+C4_PAIR = (datagen.C4A, datagen.C4B)   # "C4": inception-3a 3x3 and 5x5 branches together
+
+
+def default_sparsity(config):
+    """Headline sparsity of a config (BASELINE.json): C1 s=0.9; C3 the per-channel
+    recipe (R12); C2/C4a/C4b/C4 s=0.95 (the north star's s >= 0.95 bar)."""
+    return {"C1": 0.9, "C3": "channel"}.get(config, 0.95)
+
+
 def layers_for(config):
     if config == "C5":
         return list(datagen.C5_LAYERS), datagen.c5_weights(), datagen.C5_FIRST_SPARSITY
@@ -222,6 +231,8 @@ def run_reference(args):
         return 0
     layers, weights, s_first = layers_for(args.config)
     s = s_first if s_first is not None else args.sparsity
+    if args.config == "C4":
+        layers, weights = list(C4_PAIR), [datagen.weights(shp) for shp in C4_PAIR]
     import oracle
     oracle.build()
     flops_img = sum(per_image_flops(shp) for shp in layers)
@@ -282,6 +293,46 @@ def graph_time_us(torch, stream, fn, reps=REPS):
     return a.elapsed_time(b) * 1e3 / reps
 
 
+def rotating_time_us(torch, stream, fns, reps, prologue=False):
+    """Average device time of one call when calls rotate over the input/output
+    sets (fns[i] works on set i; the sets together exceed 2x L2, so every call
+    starts L2-cold, as the timed step does).  One CUDA graph per set.  With
+    prologue=True, fns[i]() runs a setup eagerly (e.g. stage 1 of set i before a
+    stage-2 timing, as in the step) and returns the callable to time; the setup
+    is re-run before every timed call, outside the events."""
+    graphs = []
+    with torch.cuda.stream(stream):
+        for f in fns:
+            timed = f() if prologue else f
+            if not prologue:
+                f()
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                timed()
+            graphs.append(g)
+        for g in graphs:                       # warm-up replays
+            g.replay()
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if prologue:
+            tot = 0.0
+            for i in range(reps):
+                fns[i % len(fns)]()
+                a.record(stream)
+                graphs[i % len(graphs)].replay()
+                b.record(stream)
+                b.synchronize()
+                tot += a.elapsed_time(b)
+            return tot * 1e3 / reps
+        a.record(stream)
+        for i in range(reps):
+            graphs[i % len(graphs)].replay()
+        b.record(stream)
+        b.synchronize()
+    return a.elapsed_time(b) * 1e3 / reps
+
+
 def timed_steps(torch, stream, graphs, steps, warmup, ws, dev):
     """W untimed + K timed replays (rotating over graphs), barrier + sync on both
     sides, CUDA events on the launching stream, max over ranks."""
@@ -334,19 +385,34 @@ def run_single(args, torch, dev, ws, rank, sc):
                     conv.forward(xs[si], outs[si], stream=stream)
                 graphs.append(g)
         res = {"ms_per_step": timed_steps(torch, stream, graphs, steps, warmup, ws, dev)}
-        res["compact_us"] = graph_time_us(torch, stream, lambda: conv.compact(xs[0], stream=stream))
-        res["gather_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
-        res["dense_tc_us"] = graph_time_us(torch, stream, lambda: conv.dense_forward(xs[0], outs[0], stream=stream),
-                                           reps=5)
-        res["auto_us"] = graph_time_us(torch, stream, lambda: conv.forward_auto(xs[0], outs[0], stream=stream),
-                                       reps=5)
+        del graphs
+        # per-stage and dense-path times on the same rotating sets as the step (cold L2, like the
+        # step itself); the set-0 graph replays (L2-warm) are reported beside them, labelled
+        rot = max(steps, 2 * nsets)
+        res["compact_us"] = rotating_time_us(torch, stream, [lambda i=i: conv.compact(xs[i], stream=stream)
+                                                             for i in range(nsets)], rot)
+        def stage1_then_gather(i):
+            conv.compact(xs[i], stream=stream)
+            return lambda: conv.gather(n, outs[i], stream=stream)
+
+        res["gather_us"] = rotating_time_us(torch, stream, [lambda i=i: stage1_then_gather(i) for i in range(nsets)],
+                                            rot, prologue=True)
+        res["dense_tc_us"] = rotating_time_us(torch, stream, [lambda i=i: conv.dense_forward(xs[i], outs[i],
+                                                                                             stream=stream)
+                                                              for i in range(nsets)], rot)
+        res["compact_warm_us"] = graph_time_us(torch, stream, lambda: conv.compact(xs[0], stream=stream))
+        res["gather_warm_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
+        res["dense_tc_warm_us"] = graph_time_us(torch, stream,
+                                                lambda: conv.dense_forward(xs[0], outs[0], stream=stream), reps=5)
+        res["auto_us"] = rotating_time_us(torch, stream, [lambda i=i: conv.forward_auto(xs[i], outs[i],
+                                                                                        stream=stream)
+                                                          for i in range(nsets)], rot)
         res["auto_path"] = "sparse" if conv.last_path()[0] == sc.SC_PATH_SPARSE else "dense"
         dense = sum(c[0] for c in counts) / nsets
         exact = sum(c[1] for c in counts) / nsets
         nnz = sum(c[2] for c in counts) / nsets
         res.update(dense=dense, exact=exact, nnz=nnz, exact_set0=counts[0][1], nnz_set0=counts[0][2], nsets=nsets,
                    set_mib=nsets * per_set / 2 ** 20, realized_s=1 - nnz / (n * shp.c * shp.h * shp.w))
-        del graphs
         return res
 
     return shp, n, conv, lists_per_batch, measure
@@ -360,8 +426,11 @@ def run_ours(args):
 
     peaks, peak_kind = measured_peaks()
     hbm_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    print(f"bench: rank {rank}/{ws} on {dev} ({torch.cuda.get_device_name(dev)})", file=sys.stderr, flush=True)
     if args.config == "C5":
         return run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind)
+    if args.config == "C4":
+        return run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind)
     shp, n, conv, lists_per_batch, measure = run_single(args, torch, dev, ws, rank, sc)
     s_head = args.sparsity
     clocks = ClockSampler(dev.index)
@@ -369,8 +438,8 @@ def run_ours(args):
         head = measure(s_head, args.steps, args.warmup)
         sweep = {}
         if not args.no_sweep:
-            for s in (0.9, 0.95, 0.99):
-                if abs(s - s_head) > 1e-9:
+            for s in datagen.CONFIG_SPARSITY[args.config]:
+                if s != s_head:
                     sweep[s] = measure(s, max(args.steps, 20), max(args.warmup, 3))
 
     # --- end to end through the public API with host buffers (pinned) -------------
@@ -423,12 +492,16 @@ def run_ours(args):
                      "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": measured_traffic(vname),
                      "per_launch": "2 x exact nonzero MACs of one 128-image batch",
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (unit counts x max clock)"},
-        "stages_us": {"compact": round(v["compact_us"], 3), "gather": round(v["gather_us"], 3)},
+        "stages_us": {"compact": round(v["compact_us"], 3), "gather": round(v["gather_us"], 3),
+                      "compact_l2_warm": round(v["compact_warm_us"], 3), "gather_l2_warm": round(v["gather_warm_us"], 3),
+                      "note": "compact/gather: rotating sets (L2-cold, as the step); *_l2_warm: set-0 graph replays"},
         "compact_hbm": {"achieved_gbs": round(4 * n * shp.c * shp.h * shp.w / (v["compact_us"] * 1e-6) / 1e9, 1),
                         "peak_gbs": hbm_gbs, "peak_kind": peak_kind},
-        "dense_tc": {"us": round(v["dense_tc_us"], 3), "gflops": round(gflops(v["dense"], v["dense_tc_us"] / 1e3), 2),
+        "dense_tc": {"us": round(v["dense_tc_us"], 3), "l2_warm_us": round(v["dense_tc_warm_us"], 3),
+                     "gflops": round(gflops(v["dense"], v["dense_tc_us"] / 1e3), 2),
                      "sparse_speedup": round(v["dense_tc_us"] / (v["ms_per_step"] * 1e3), 3),
-                     "note": "in-library tcgen05 TF32 implicit-GEMM conv (dense_conv_forward) on the same batch"},
+                     "note": "in-library tcgen05 TF32 implicit-GEMM conv (dense_conv_forward) on the same batch, "
+                             "same rotating sets (L2-cold) as the sparse step"},
         "sweep": {str(s): {"value": round(gflops(r["dense"], r["ms_per_step"]), 2),
                            "nonzero_mac_per_s": round(r["exact"] * ws / (r["ms_per_step"] * 1e-3), 1),
                            "ms_per_step": round(r["ms_per_step"], 5),
@@ -553,6 +626,97 @@ def run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
     return 0
 
 
+def run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
+    """C4 = C4a + C4b (inception-3a 3x3 and 5x5 branches, BASELINE.json configs[3]) run
+    together on two streams, as SURVEY 8d asks: a step = both sparse forwards on this
+    rank's 128 images, forked from and joined into one stream, one CUDA graph per
+    rotating input set (weak scaling over ranks)."""
+    s = args.sparsity
+    shps = C4_PAIR
+    n = shps[0].n
+    convs = []
+    for shp in shps:
+        w, b = datagen.weights(shp)
+        convs.append(sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), n, shp.c, shp.h, shp.w,
+                                   shp.stride, shp.pad, shp.groups))
+    main = torch.cuda.Stream(dev)
+    side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    per_set = sum(4 * n * (shp.c * shp.h * shp.w + shp.k * shp.ho * shp.wo) for shp in shps)
+    nsets = max(2, -(-2 * max(l2_bytes, 126 * 2 ** 20) // per_set))
+    xs, outs, counts = [], [], []
+    for si in range(nsets):
+        start = shard.image_start(si, rank, ws, n)
+        xs.append([torch.from_numpy(datagen.activations(shp, s, start=start, count=n)).to(dev) for shp in shps])
+        outs.append([torch.empty((n, shp.k, shp.ho, shp.wo), device=dev) for shp in shps])
+        counts.append([mac_counts(x, shp) for x, shp in zip(xs[-1], shps)])
+
+    def step(si):  # fork both layers off `main`, join back
+        ev = torch.cuda.Event()
+        ev.record(main)
+        for j in range(2):
+            side[j].wait_event(ev)
+            convs[j].forward(xs[si][j], outs[si][j], stream=side[j])
+            done = torch.cuda.Event()
+            done.record(side[j])
+            main.wait_event(done)
+
+    graphs = []
+    with torch.cuda.stream(main):
+        for si in range(nsets):
+            step(si)
+        main.synchronize()
+        for si in range(nsets):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=main, capture_error_mode="relaxed"):
+                step(si)
+            graphs.append(g)
+    clocks = ClockSampler(dev.index)
+    with clocks:
+        ms = timed_steps(torch, main, graphs, args.steps, args.warmup, ws, dev)
+        alone = [rotating_time_us(torch, main, [lambda i=i, j=j: convs[j].forward(xs[i][j], outs[i][j], stream=main)
+                                               for i in range(nsets)], max(args.steps, 2 * nsets))
+                 for j in range(2)]
+        dense_alone = [rotating_time_us(torch, main, [lambda i=i, j=j: convs[j].dense_forward(xs[i][j], outs[i][j],
+                                                                                             stream=main)
+                                                     for i in range(nsets)], max(args.steps, 2 * nsets))
+                       for j in range(2)]
+    del graphs
+    dense = sum(c[0] for cs in counts for c in cs) / nsets
+    exact = sum(c[1] for cs in counts for c in cs) / nsets
+    nbytes = sum(algorithmic_bytes(shp, n, sum(cs[j][2] for cs in counts) / nsets,
+                                   n * convs[j].lists(1)["tiles"] * shp.c) for j, shp in enumerate(shps))
+    t_fp32, t_hbm, t_roof = roofline_times(exact, nbytes, hbm_gbs)
+    value = 2 * dense * ws / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C4 = C4a + C4b on two streams: {workload_name(shps[0], s, n)}; "
+                               f"{workload_name(shps[1], s, n)}",
+                   "global_batch": n * ws, "parallelism": f"dp{ws}",
+                   "l2": f"{nsets} rotating input/output sets ({nsets * per_set / 2 ** 20:.0f} MiB > 2x L2)",
+                   "timing": "CUDA events around K graph replays (both layers forked onto two streams), max over ranks",
+                   "variants": [c.variant[1] for c in convs]},
+        "nonzero_mac_per_s": round(exact * ws / (ms * 1e-3), 1),
+        "pct_roofline": round(100 * t_roof / (ms * 1e-3), 2),
+        "roofline_step": {"t_roof_us": round(t_roof * 1e6, 3), "t_fp32_us": round(t_fp32 * 1e6, 3),
+                          "t_hbm_us": round(t_hbm * 1e6, 3), "bytes": int(nbytes), "bound": "hbm" if t_hbm > t_fp32
+                          else "alu", "exact_nonzero_macs": int(exact), "dense_macs": int(dense)},
+        "layers_alone_us": {"C4a": round(alone[0], 2), "C4b": round(alone[1], 2)},
+        "dense_tc": {"us_sequential": round(sum(dense_alone), 3), "C4a_us": round(dense_alone[0], 2),
+                     "C4b_us": round(dense_alone[1], 2),
+                     "sparse_speedup": round(sum(dense_alone) / (ms * 1e3), 3),
+                     "note": "in-library tcgen05 TF32 dense conv of both layers back to back, same rotating sets"},
+        "gpu_launches": int(args.steps * sum(c.launch_counts[0] for c in convs)),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    shard.finalize(ws)
+    return 0
+
+
 # Paper Table 3 (PAPER.md:161-170): Xeon E5-2630v4 CPU, Caffe+MKL GEMM vs ISC, ms and printed speedup.
 # Context only (another machine, batch size unstated).
 PAPER_TABLE3 = {"LeNet-Conv2": (0.854, 0.123, 6.96), "AlexNetC-Conv3": (0.329, 0.122, 2.69),
@@ -666,26 +830,100 @@ def run_backward(args):
     return 0
 
 
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` with N > 1 outside torchrun: start N ranks on this node
+    (one process per GPU, NCCL over 127.0.0.1) with the same arguments; rank 0
+    prints the line.  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench: launching {args.gpus} ranks: {' '.join(cmd[1:])}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def run_stub(args):
+    """CPU stand-in for the GPU arm (tests only: `--cpu-stub`, gloo): the same rank
+    orchestration -- shard by image (C5: the 1024-image batch split over ranks;
+    others: each rank its own batch), W untimed + K timed steps between barriers,
+    max over ranks of the elapsed time, one JSON line from rank 0 -- around a stub
+    step (a nonzero count of the rank's images: no arithmetic of the method)."""
+    import torch.distributed as dist
+    ws, rank, _ = shard.dist_env()
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("gloo")
+    layers, _, s_first = layers_for(args.config if args.config != "C4" else "C4a")
+    s = s_first if s_first is not None else args.sparsity
+    shp = layers[0]
+    if args.config == "C5":
+        lo, hi = shard.shard_range(shp.n, rank, ws)
+        scaling, global_batch = "strong", shp.n
+    else:
+        lo = shard.image_start(0, rank, ws, shp.n)
+        hi = lo + shp.n
+        scaling, global_batch = "weak", shp.n * ws
+    x = datagen.activations(shp, s, start=lo, count=min(hi - lo, 8))   # a bounded slice: orchestration only
+
+    def step():
+        return int(np.count_nonzero(x))
+
+    for _ in range(args.warmup):
+        step()
+    shard.barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = shard.max_over_ranks(time.perf_counter() - t0, ws)
+    images = shard.sum_over_ranks(hi - lo, ws)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": round(images * args.steps / el, 3), "unit": "stub images/s",
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(1e3 * el / args.steps, 5), "higher_is_better": True,
+                          "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "stub": "cpu orchestration test (no GPU work; not a benchmark number)",
+                          "config": {"workload": args.config, "global_batch": global_batch,
+                                     "images_per_step": int(images), "parallelism": f"dp{ws}"}}), flush=True)
+    shard.finalize(ws)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS) + ["C5"])
-    ap.add_argument("--sparsity", type=float, default=0.95)
+    ap.add_argument("--config", default="C2", choices=sorted(datagen.CONFIGS) + ["C4", "C5"])
+    ap.add_argument("--sparsity", default=None,
+                    help="input sparsity (default per config: C1 0.9, C3 'channel', else 0.95)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--table2", action="store_true", help="paper Table 2 layers: sparse vs dense on B200")
     ap.add_argument("--table2-batch", type=int, default=128)
     ap.add_argument("--backward", action="store_true", help="f4: sparse backward vs library dense backward")
+    ap.add_argument("--cpu-stub", action="store_true", help=argparse.SUPPRESS)   # tests: orchestration on CPU
     args = ap.parse_args()
+    if args.sparsity is None:
+        args.sparsity = default_sparsity(args.config)
+    elif args.sparsity != "channel":
+        args.sparsity = float(args.sparsity)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and ws_env is None:
+        return relaunch_under_torchrun(args)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench: WORLD_SIZE={ws_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.backward:
         return run_backward(args)
     if args.table2:
         return run_table2(args)
     if args.warmup < 3:
         args.warmup = 3
+    if args.cpu_stub:
+        return run_stub(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
