@@ -61,12 +61,30 @@ def measured_peaks():
 
 
 def measured_traffic(variant_name):
-    """DRAM bytes per gather launch from the committed ncu capture (or None)."""
+    """Traffic figures of one gather launch from the committed ncu capture
+    (profiles/gather_traffic.json): dict(traffic_bytes, dram_bytes, l2_write_bytes,
+    l2_to_sm_bytes) or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "gather_traffic.json")) as f:
-            return json.load(f).get(variant_name)
+            t = json.load(f).get(variant_name)
     except OSError:
         return None
+    return t if isinstance(t, dict) else None
+
+
+def measured_fma_census(workload):
+    """Hardware FFMA/FFMA2 census of the gather for `workload` ("C2 s=0.95") from the
+    committed ncu run (profiles/r2_fma_census.json, tools/fma_census.py) or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_fma_census.json")) as f:
+            rows = json.load(f)["workloads"]
+    except (OSError, KeyError, ValueError):
+        return None
+    for r in rows:
+        if r["workload"] == workload:
+            return {k: r[k] for k in ("executed_lane_fmas", "exact_nonzero_macs", "dense_macs", "wasted_fma_factor",
+                                      "skipped_vs_dense_exact", "skipped_vs_dense_executed")}
+    return None
 
 
 # ------------------------------------------------------------------ counting
@@ -489,9 +507,13 @@ def run_ours(args):
                           "exact_nonzero_macs": int(v["exact"]), "dense_macs": int(v["dense"])},
         "roofline": {"kernel": f"gather (stage 2, {vname})", "bound": "alu", "achieved": round(achieved, 3),
                      "peak": round(FP32_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
-                     "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": measured_traffic(vname),
+                     "frac": round(achieved / FP32_PEAK_TFLOPS, 4),
+                     "traffic": (measured_traffic(vname) or {}).get("traffic_bytes"),
+                     "traffic_detail": measured_traffic(vname),
                      "per_launch": "2 x exact nonzero MACs of one 128-image batch",
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (unit counts x max clock)"},
+        "fma_census": measured_fma_census(f"{args.config} s={s_head}"),
+        "wasted_fma_factor": (measured_fma_census(f"{args.config} s={s_head}") or {}).get("wasted_fma_factor"),
         "stages_us": {"compact": round(v["compact_us"], 3), "gather": round(v["gather_us"], 3),
                       "compact_l2_warm": round(v["compact_warm_us"], 3), "gather_l2_warm": round(v["gather_warm_us"], 3),
                       "note": "compact/gather: rotating sets (L2-cold, as the step); *_l2_warm: set-0 graph replays"},
