@@ -45,6 +45,16 @@ namespace fast {
 namespace sc {
 namespace fast {
 
+inline int sm_count() {
+    static const int sms = [] {
+        int d = 0, v = 148;
+        if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
+            v = 148;
+        return v;
+    }();
+    return sms;
+}
+
 template <class V>
 cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs, const float* wpack,
                      const float* bias, float* out, uint2* rowlist, uint32_t* rowcnt, cudaStream_t st, Gate gate) {
@@ -73,6 +83,7 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
+    a.edge_last = grid >= 2LL * sm_count() * V::MINB ? 1 : 0;
     if (gate.flag != nullptr) {
         if (rowlist != nullptr) return cudaErrorNotSupported;
         auto kg = gather_fast_kernel<V, false, ArgsGated>;

@@ -32,6 +32,7 @@ struct Args {
     int n, C, H, K, Cg, Kg, kblocks, Ho, relu;
     int64_t cap;
     int ytiles, units, ctas_per_kb;
+    int edge_last;     // unit order: interior row tiles first, edge tiles last (grids of >= 2 waves)
 };
 // f3 (device-side path selection) launches a separate instantiation with the gate
 // appended: adding the field to Args itself was measured to slow the ungated
@@ -146,9 +147,31 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     }
     if (!active) return;
 
-    const int n = unit / a.ytiles;
-    const int y0 = (unit % a.ytiles) * TY;
-    const int64_t stream = (int64_t)unit;  // = n * tiles + tile (ytiles == tiles)
+    // Unit order (edge_last): interior row tiles first, then every image's first tile, then
+    // its last tile.  The edge tiles' input windows are clipped by the padding (C2: 3 and 2 of 4
+    // window rows), so their streams are shorter; consecutive units share a CTA whose
+    // warps walk the weight ring in lock step, so grouping by tile position keeps short
+    // streams from idling in CTAs of long ones, and the short CTAs run last (measured: C5 -7%,
+    // C2 (1.66 waves) +2%, hence only for grids of >= 2 waves).  A relabelling only: every
+    // stream is computed the same way by whichever warp owns it.
+    int n, tile;
+    {
+        const int nimg = a.n, T = a.ytiles;
+        const int inner = T > 2 ? nimg * (T - 2) : 0;
+        if (!a.edge_last) {
+            n = unit / T;
+            tile = unit - n * T;
+        } else if (unit < inner) {
+            n = unit % nimg;
+            tile = 1 + unit / nimg;
+        } else {
+            const int e = unit - inner;
+            n = e % nimg;
+            tile = T > 2 ? (e < nimg ? 0 : T - 1) : e / nimg;
+        }
+    }
+    const int y0 = tile * TY;
+    const int64_t stream = (int64_t)n * a.ytiles + tile;
     const uint2* sbase = a.entries + stream * a.cap;
     const uint32_t* of = a.offs + stream * (a.C + 1) + (int64_t)g * a.Cg;  // of[cl] = marker of channel g*Cg+cl
     uint64_t* pbar = pbar_all + warp * V::SLOTS;

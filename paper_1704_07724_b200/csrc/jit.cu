@@ -476,6 +476,12 @@ cudaError_t launch(void* fn, size_t smem, const Params& p, const Geometry& g, in
     a.ytiles = (int)g.tiles;
     a.units = (int)n * a.ytiles;
     a.ctas_per_kb = (a.units + p.NW - 1) / p.NW;
+    {
+        int d = 0, sms = 148;
+        if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
+            sms = 148;
+        a.edge_last = (int64_t)a.ctas_per_kb * g.G * g.kblocks >= 2LL * sms * p.MINB ? 1 : 0;
+    }
     ag.gate = gate;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
     void* pa = gate.flag ? static_cast<void*>(&ag) : static_cast<void*>(&a);
