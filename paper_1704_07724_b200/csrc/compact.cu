@@ -379,6 +379,59 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
     const unsigned shift_t = (unsigned)(lo * W);  // code = flat index - i_lo*W
     uint2* st_t = entries + ((int64_t)n * tiles + (lane < tiles ? lane : 0)) * cap;
+    if constexpr (!FROM_ROWS) {
+        // Lanes over the plane's list entries: entry k (row i) goes to every tile whose window
+        // holds row i, at that tile's marker index + 1 + (k - first list entry of the window);
+        // lanes over tiles write the markers.  Row i of an entry from its flat index through a
+        // float reciprocal (exact: the quotient's fraction stays >= 0.5/W from an integer).
+        // Lane r < H: the first tile whose window holds row r, and the last.
+        const int num = lane + P - NWR;
+        const int tl_r = num < 0 ? 0 : num / TYT + 1;
+        const int th_r0 = (lane + P) / TYT;
+        const int th_r = th_r0 < tiles - 1 ? th_r0 : tiles - 1;
+        const int span = (NWR + TYT - 1) / TYT;  // tiles holding one row, at most
+        const float invW = 1.0f / (float)W;
+#pragma unroll
+        for (int q = 0; q < kPerWarp; ++q) {
+            const int ch = warp + q * kPlaneWarps;
+            if (ch >= nch) break;
+            const int plane = n * C + c0 + ch;
+            const uint2* lst = plist + (int64_t)plane * HW;
+            const uint32_t pre = pv[q];
+            const uint32_t a = __shfl_sync(0xffffffffu, pre, r0), b = __shfl_sync(0xffffffffu, pre, r1);
+            const uint32_t cnt_t = (lane < tiles && r1 > r0) ? b - a : 0u;
+            const uint32_t pos_t = lane < tiles ? start_s[lane][ch] : 0u;
+            const uint32_t pnext = __shfl_down_sync(0xffffffffu, pre, 1);
+            const unsigned rowbits = __ballot_sync(0xffffffffu, lane < H && pnext > pre);
+            unsigned mask_t = 0;
+            const uint64_t rb64 = (uint64_t)rowbits << 32;
+            for (int ty = 0; ty < TY; ++ty) {
+                const int sh = 32 + lo + ty * T;
+                if (sh < 64) mask_t |= (unsigned)(rb64 >> sh);
+            }
+            mask_t &= (1u << R) - 1u;
+            if (cnt_t > 0) st_t[pos_t] = make_uint2((unsigned)(c0 + ch), (unsigned)NWIN + mask_t);
+            const uint32_t total = __shfl_sync(0xffffffffu, pre, H);
+            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                const bool live = k < total;
+                uint2 e = en0[q];
+                if (k0 > 0 && live) e = __ldg(lst + k);
+                const int i = live ? __float2int_rz(((float)e.y + 0.5f) * invW) : 0;
+                const int tl = __shfl_sync(0xffffffffu, tl_r, i);
+                const int th = __shfl_sync(0xffffffffu, th_r, i);
+                for (int j = 0; j < span; ++j) {
+                    const int t = tl + j <= th ? tl + j : th;  // every lane takes part in the shuffles
+                    const uint32_t at = __shfl_sync(0xffffffffu, a, t);
+                    const uint32_t pt = __shfl_sync(0xffffffffu, pos_t, t);
+                    const unsigned sh = __shfl_sync(0xffffffffu, shift_t, t);
+                    if (live && tl + j <= th)
+                        entries[((int64_t)n * tiles + t) * cap + pt + 1 + (k - at)] = make_uint2(e.x, e.y - sh);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < kPerWarp; ++q) {
         const int ch = warp + q * kPlaneWarps;
