@@ -20,3 +20,7 @@ python tools/prof_run.py C2 0.95 1 > gpurun_out/m/plain_prof.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:gather_fast -c 1 -o gpurun_out/m/gather_C2 python tools/prof_run.py C2 0.95 1 > gpurun_out/m/ncu_gather.log 2>&1; echo ncu_gather=$?
 python tools/dense_probe.py > gpurun_out/m/plain_dense.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:dense_tc -c 1 -o gpurun_out/m/dense_C2 python tools/dense_probe.py > gpurun_out/m/ncu_dense.log 2>&1; echo ncu_dense=$?
+timeout 900 python bench.py --table2 > gpurun_out/m/table2.log 2>&1; echo table2=$?
+timeout 600 python bench.py --backward --steps 20 --warmup 3 > gpurun_out/m/bench_bwd.log 2>&1; echo bwd=$?
+timeout 300 python tools/crossover_curve.py C2 C4a C4b > gpurun_out/m/crossover.txt 2>&1; echo crossover=$?
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/m/smoke.log 2>&1; echo smoke=$?
