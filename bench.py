@@ -546,6 +546,18 @@ def run_ours(args):
         "gpu_launches": int(args.steps * conv.launch_counts[0]),
         "clocks": clocks.summary(),
     }
+    # the gather also against the in-run FP32 pipe probe and the observed clock
+    try:
+        probe = {"ffma_lane_fma_per_clk_sm": round(sc.probe_fma(0), 2),
+                 "ffma2_lane_fma_per_clk_sm": round(sc.probe_fma(1), 2)}
+        mhz = line["clocks"].get("sm_mhz") or F_MAX_GHZ * 1e3
+        best = max(probe.values())
+        peak_probe = SM_COUNT * best * 2 * mhz * 1e6 / 1e12
+        probe.update(clock_mhz=mhz, peak_tflops=round(peak_probe, 2), frac=round(achieved / peak_probe, 4),
+                     note="peak = 148 SMs x the best probed lane-FMA/clk x 2 flop x the median SM clock seen")
+        line["roofline"]["vs_probe"] = probe
+    except Exception as exc:  # the probe is context only
+        line["roofline"]["vs_probe"] = {"error": str(exc)[:120]}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, imgs, secs = cpu_oracle_rate([shp], datagen.activations(shp, s_head, start=0, count=min(n, 16)),
                                            [datagen.weights(shp)])
