@@ -1,4 +1,4 @@
-"""Refresh profiles/ from a gpurun_out/ produced by tools/gpu_final.sh:
+"""Refresh profiles/ from a gpurun_out/ produced by tools/gpu_calls/gpu_final.sh:
 launch list, gather/compaction ncu summaries, gather DRAM traffic, bench lines."""
 import csv
 import json
