@@ -422,6 +422,19 @@ def run_single(args, torch, dev, ws, rank, sc):
         res["gather_warm_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
         res["dense_tc_warm_us"] = graph_time_us(torch, stream,
                                                 lambda: conv.dense_forward(xs[0], outs[0], stream=stream), reps=5)
+        # context only: the library convolution of torch (cuDNN), exact FP32 and TF32
+        wd = torch.from_numpy(w).to(dev)
+        bd = torch.from_numpy(b).to(dev)
+
+        def cudnn(i, tf32):
+            torch.backends.cudnn.allow_tf32 = tf32
+            torch.nn.functional.conv2d(xs[i], wd, bd, stride=shp.stride, padding=shp.pad, groups=shp.groups)
+
+        for tf32 in (False, True):
+            torch.backends.cudnn.allow_tf32 = tf32
+            res[f"cudnn_{'tf32' if tf32 else 'fp32'}_us"] = rotating_time_us(
+                torch, stream, [lambda i=i, t=tf32: cudnn(i, t) for i in range(nsets)], rot)
+        torch.backends.cudnn.allow_tf32 = True
         res["auto_us"] = rotating_time_us(torch, stream, [lambda i=i: conv.forward_auto(xs[i], outs[i],
                                                                                         stream=stream)
                                                           for i in range(nsets)], rot)
@@ -524,6 +537,9 @@ def run_ours(args):
                      "sparse_speedup": round(v["dense_tc_us"] / (v["ms_per_step"] * 1e3), 3),
                      "note": "in-library tcgen05 TF32 implicit-GEMM conv (dense_conv_forward) on the same batch, "
                              "same rotating sets (L2-cold) as the sparse step"},
+        "cudnn_context": {"fp32_us": round(v["cudnn_fp32_us"], 3), "tf32_us": round(v["cudnn_tf32_us"], 3),
+                          "note": "torch.nn.functional.conv2d (cuDNN) on the same rotating sets; context only, not "
+                                  "part of the library"},
         "sweep": {str(s): {"value": round(gflops(r["dense"], r["ms_per_step"]), 2),
                            "nonzero_mac_per_s": round(r["exact"] * ws / (r["ms_per_step"] * 1e-3), 1),
                            "ms_per_step": round(r["ms_per_step"], 5),
