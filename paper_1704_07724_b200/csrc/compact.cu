@@ -237,6 +237,9 @@ template <int NSLOT, int IMG>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     const float* __restrict__ in, int nimg, int C, int H, int W, int TYT, int P, int NWR, int tiles,
     uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow, Gate gate) {
+    // the emit kernel (a programmatic dependent on the forward path) may be scheduled once every
+    // CTA of this grid is resident; it waits for this grid's completion before reading
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (gate_closed(gate)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // grid (channel blocks, images): no division to split a plane index
@@ -316,6 +319,9 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     // completion before it reads the streams
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (gate_closed(gate)) return;
+    // launched as a programmatic dependent of the count kernel (FROM_ROWS: of the tile-count
+    // kernel, or plainly): its lists are read only from here on (a no-op without the attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
     extern __shared__ uint2 rowbuf_s[];  // FROM_ROWS: [kPlaneWarps][H*W]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -559,15 +565,28 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     if (e != cudaSuccess) return e;
     const int ch = emit_chunk(g, n);
     const int chunks = (int)((g.C + ch - 1) / ch);
+    // a programmatic dependent of the count kernel: its launch and CTA placement overlap the
+    // count kernel's last wave
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n * chunks));
+    cfg.blockDim = dim3(kPlaneWarps * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint2* cplist = plist;
+    const uint32_t* cprow = prow;
+    const uint32_t* ccnt = cnt;
     if (ch == 32)
-        compact_plane_emit_kernel<false, 32><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
-            plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-            (int)g.tiles, g.cap, chunks, entries, offs, gate);
-    else
-        compact_plane_emit_kernel<false, 16><<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
-            plist, prow, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
-            (int)g.tiles, g.cap, chunks, entries, offs, gate);
-    return cudaGetLastError();
+        return cudaLaunchKernelEx(&cfg, compact_plane_emit_kernel<false, 32>, cplist, cprow, ccnt, (int)g.C, (int)g.H,
+                                  (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, (int)g.tiles, g.cap,
+                                  chunks, entries, offs, gate);
+    return cudaLaunchKernelEx(&cfg, compact_plane_emit_kernel<false, 16>, cplist, cprow, ccnt, (int)g.C, (int)g.H,
+                              (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, (int)g.tiles, g.cap,
+                              chunks, entries, offs, gate);
 }
 
 // cnt[n][t][c] = row counts summed over tile t's window rows (chained consumers)
