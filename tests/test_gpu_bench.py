@@ -41,3 +41,18 @@ def test_bench_reference_arm():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_pair_config_two_streams():
+    """C4 = C4a + C4b forked onto two streams: one line, both layers' work."""
+    d = run_bench("--config", "C4", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["scaling"] == "weak"
+    assert set(d["layers_alone_us"]) == {"C4a", "C4b"}
+    assert d["roofline_step"]["dense_macs"] > 0 and d["dense_tc"]["us_sequential"] > 0
+
+
+def test_bench_chain_config_strong_scaling_line():
+    """C5 (the scaling config): the 1024-image chain on the ranks present (here one)."""
+    d = run_bench("--config", "C5", "--gpus", "1", "--steps", "1", "--warmup", "3", "--no-cpu-baseline")
+    assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["config"]["global_batch"] == 1024
+    assert len(d["layers_unfused_us"]) == 3 and d["e2e"]["h2d_bytes_per_step"] > 0
