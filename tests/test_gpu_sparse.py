@@ -35,7 +35,7 @@ def make_conv(sc, shp, w, b, relu=False, max_batch=None):
 # Tile height the stage-2 stream layout uses for each BASELINE config (the shipped
 # variants): stated here so a plan that silently changed its
 # layout fails the stream check instead of being compared against itself.
-EXPECTED_TY = {"C1": 6, "C2": 2, "C3": 3, "C4a": 1, "C4b": 4}
+EXPECTED_TY = {"C1": 1, "C2": 2, "C3": 3, "C4a": 2, "C4b": 3}
 
 
 def check_lists(conv, x, n, cfg=None):
@@ -292,11 +292,12 @@ def test_c5_chain_per_layer(sc):
 # and the superseded round-1 tilings (tools/gen_gather.py SUPERSEDED: no longer built into the
 # library), generated at run time through SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE".
 JIT_TILINGS = {1: "7,2,7,1,8,4,3,254", 2: "3,2,7,1,8,4,3,254", 3: "2,2,7,1,4,4,3,254", 4: "2,2,7,1,4,4,3,254",
+               5: "6,2,7,1,4,4,3,254", 28: "1,4,11,1,16,2,3,254", 29: "4,1,11,1,16,2,3,254",
                7: "7,1,11,1,16,4,3,254", 10: "3,3,11,1,8,4,3,254", 11: "3,4,7,1,8,3,3,254",
                12: "2,4,11,1,8,3,3,254", 13: "5,2,11,1,8,4,3,254", 14: "1,4,11,1,8,3,3,254",
                30: "2,1,11,1,16,2,3,254"}
-FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28)] +
-          [("C4b", v) for v in (0, 4, 29, 30)] + [("C3", v) for v in (0, 3, 33)])
+FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28, 51)] +
+          [("C4b", v) for v in (0, 4, 29, 30, 52)] + [("C3", v) for v in (0, 3, 33)] + [("C1", v) for v in (0, 5, 50)])
 
 
 def force_kernel(monkeypatch, variant):

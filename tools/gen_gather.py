@@ -38,13 +38,15 @@ OUT = os.path.join(ROOT, "paper_1704_07724_b200", "csrc", "gather_variants.inc")
 # NW compute warps (+1 producer warp) per CTA, MINB CTAs per SM (register budget
 # 65536 / (32*(NW+1)*MINB)).
 VARIANTS = [
-    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 (LeNet conv2)
     # k-quads, 3 warps/SMSP, 16-channel weight chunks in a 2-stage ring: measured best of the
     # CH/STAGES/SLOTS/PIECE sweep
     (21, "r3s3p1_w13_ty2_kl4_nw11_ch16s2", 3, 3, 1, 13, 2, 4, 11, 1, 16, 2),   # C2, C5 (AlexNet conv3/4/5)
-    (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a (inception-3a 3x3)
-    (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b: 32 channels = one warp
     (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
+    # round 2: best of whole-forward sweeps (stage 1 depends on the tile height too;
+    # profiles/r2_jit_tune_*.txt), replacing V5 / V28 / V29
+    (50, "r5s5p0_w12_ty1_kl1_nw4_ch10", 5, 5, 0, 12, 1, 1, 4, 1, 10, 2),     # C1: x-pairs, 4 warps per CTA
+    (51, "r3s3p1_w28_ty2_kl2_nw11_ch32", 3, 3, 1, 28, 2, 2, 11, 1, 32, 2),   # C4a: k-pairs
+    (52, "r5s5p2_w28_ty3_kl1_nw11", 5, 5, 2, 28, 3, 1, 11, 1, 16, 2),        # C4b: x-pairs
     # paper Table 2 shapes: stride 2, 1x1, small planes
     # (parameters from tools/jit_tune.py sweeps of run-time generated variants, profiles/r1_jit_tune_t2.txt)
     (40, "r5s5p1t2_w11_ty2_kl2_sl2p126", 5, 5, 1, 11, 2, 2, 11, 1, 16, 2, None, 2, 126, 2),  # LeNet-Conv2 (T=2)
@@ -64,6 +66,9 @@ VARIANTS = [
 # into libsparseconv.so; any of them can be generated at run time for tuning or tests with
 # SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE" (csrc/jit.cu).
 SUPERSEDED = [
+    (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 until round 2
+    (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a until round 2
+    (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b until round 2
     (1, "r3s3p1_w13_ty7_kl2", 3, 3, 1, 13, 7, 2, 7, 1, 8, 4),      # C2
     (2, "r3s3p1_w28_ty3_kl2", 3, 3, 1, 28, 3, 2, 7, 1, 8, 4),      # C4a
     (3, "r5s5p2_w27_ty2_kl2", 5, 5, 2, 27, 2, 2, 7, 1, 4, 4),      # C3
@@ -82,7 +87,7 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 28, 29, 33, 48, 49]  # 48/49 need Kg >= KMIN
+PRIORITY = [21, 51, 52, 33, 50, 48, 49]  # 48/49 need Kg >= KMIN
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):

@@ -49,7 +49,7 @@ if os.environ.get("TUNE_GRID"):  # "2:4,1:4" = (TY, KL) pairs
     grid = [tuple(int(u) for u in t.split(":")) for t in os.environ["TUNE_GRID"].split(",")]
 nws, chs, stages = env_list("TUNE_NWS", nws), env_list("TUNE_CHS", chs), env_list("TUNE_STAGES", stages)
 slots, pieces = env_list("TUNE_SLOTS", slots), env_list("TUNE_PIECES", pieces)
-full = cfg.startswith("T2:")  # Table 2 layers: time the whole forward (the tile height changes stage 1 too)
+full = cfg.startswith("T2:") or bool(os.environ.get("TUNE_FULL"))  # time the whole forward (the tile height changes stage 1 too)
 os.environ.pop("SC_JIT_FORCE", None)
 base = sc.SparseConv(torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), shp.n, shp.c, shp.h, shp.w,
                      shp.stride, shp.pad, shp.groups)
