@@ -18,6 +18,8 @@ cfg, s = sys.argv[1], (sys.argv[2] if sys.argv[2] == "channel" else float(sys.ar
 quick = len(sys.argv) > 3
 if cfg.startswith("T2:"):  # a paper Table 2 layer by name, N=128
     shp = {t.name: t for t, _ in datagen.table2_shapes(n=128)}[cfg[3:]]
+elif cfg.startswith("C5."):  # a layer of the C5 chain (i.i.d. input at s), N from TUNE_N (default 256)
+    shp = datagen.C5_LAYERS[int(cfg[3:])].with_batch(int(os.environ.get("TUNE_N", "256")))
 else:
     shp = datagen.CONFIGS[cfg]
 w, b = datagen.weights(shp)
