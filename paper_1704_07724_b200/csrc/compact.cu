@@ -553,8 +553,10 @@ cudaError_t launch_plane_lists(const Geometry& g, int64_t n, const float* in, ui
 
 // Channels per emit CTA: 32 (measured best on C2: 1024 CTAs), 16 when 32 would leave fewer
 // than four CTAs per SM (C4a / C3: 384 -> 768 CTAs, compaction 31 -> 30 and 32 -> 30 us).
+// ... and 8 channels when 16 would leave fewer than two CTAs per SM (few channels per image: C1, C4b)
 static int emit_chunk(const Geometry& g, int64_t n) {
-    return n * ((g.C + 31) / 32) >= 4 * 148 ? 32 : 16;
+    if (n * ((g.C + 31) / 32) >= 4 * 148) return 32;
+    return n * ((g.C + 15) / 16) >= 2 * 148 ? 16 : 8;
 }
 
 cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32_t* cnt, uint2* plist,
@@ -580,6 +582,10 @@ cudaError_t launch_compact(const Geometry& g, int64_t n, const float* in, uint32
     const uint2* cplist = plist;
     const uint32_t* cprow = prow;
     const uint32_t* ccnt = cnt;
+    if (ch == 8)
+        return cudaLaunchKernelEx(&cfg, compact_plane_emit_kernel<false, 8>, cplist, cprow, ccnt, (int)g.C, (int)g.H,
+                                  (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, (int)g.tiles, g.cap,
+                                  chunks, entries, offs, gate);
     if (ch == 32)
         return cudaLaunchKernelEx(&cfg, compact_plane_emit_kernel<false, 32>, cplist, cprow, ccnt, (int)g.C, (int)g.H,
                                   (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin, (int)g.tiles, g.cap,
@@ -616,7 +622,8 @@ cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt
     const int ch = emit_chunk(g, n);
     const int chunks = (int)((g.C + ch - 1) / ch);
     const size_t smem = sizeof(uint2) * kPlaneWarps * g.H * g.W;
-    auto kern = ch == 32 ? compact_plane_emit_kernel<true, 32> : compact_plane_emit_kernel<true, 16>;
+    auto kern = ch == 32 ? compact_plane_emit_kernel<true, 32>
+                         : (ch == 16 ? compact_plane_emit_kernel<true, 16> : compact_plane_emit_kernel<true, 8>);
     if (smem > 48 * 1024) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
