@@ -220,12 +220,12 @@ static cudaError_t launch_compact_streamwise(const Geometry& g, int64_t n, const
 //         order), (b) the exclusive row prefix prow[plane][r] = nonzeros
 //         before row r (lane r: popc of the ballot bits below r*W), and (c)
 //         each tile's window count cnt[n][t][c] = prow[r1] - prow[r0].
-//  emit:  one CTA per (image, chunk of 32 channels).  Warp w scans tiles
+//  emit:  one CTA per (image, chunk of 8/16/32 channels).  Warp w scans tiles
 //         w, w+NW, ...: the chunk's stream base is (count ? 1 + count : 0) summed over the
 //         channels before it, a shuffle scan over the chunk's channels gives
-//         each marker index (-> offs).  Then each warp flattens, per plane,
-//         the (tile, marker / entry) writes into one work list (scan over the
-//         tiles' run lengths) so every lane stores one 8-byte entry per step.
+//         each marker index (-> offs).  Then, per plane, lanes over tiles write the
+//         markers and lanes over the plane's list entries write each entry into every
+//         tile stream whose window holds its row.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr int kMaxSlots = 32;     // plane elements / 32 on the plane-major path
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
 
 // FROM_ROWS (chained layers, f1): the plane lists come from the producing gather as
 // per-(plane, row) slots rows[plane*H + r][0..W) with counts rcnt[plane*H + r]
-// (entries (bits, flat index)); each warp first gathers a plane's rows into a
-// contiguous shared list and derives the row prefix from the counts.
+// (entries (bits, flat index)); each warp derives the plane's row prefix from the counts
+// and finds an entry's row by a search over that prefix.
 template <bool FROM_ROWS, int kPlaneChunk>
 __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const uint2* __restrict__ plist, const uint32_t* __restrict__ prow, const uint32_t* __restrict__ cnt, int C,
@@ -323,7 +323,6 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     // kernel, or plainly): its lists are read only from here on (a no-op without the attribute)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ uint32_t start_s[kMaxTiles][kPlaneChunk];
-    extern __shared__ uint2 rowbuf_s[];  // FROM_ROWS: [kPlaneWarps][H*W]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int chunk = blockIdx.x % chunks;
     const int n = blockIdx.x / chunks;
@@ -385,11 +384,13 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
     const int r0 = lo < 0 ? 0 : (lo > H ? H : lo), r1 = (lo + NWR < H) ? (lo + NWR < 0 ? 0 : lo + NWR) : H;
     const unsigned shift_t = (unsigned)(lo * W);  // code = flat index - i_lo*W
     uint2* st_t = entries + ((int64_t)n * tiles + (lane < tiles ? lane : 0)) * cap;
-    if constexpr (!FROM_ROWS) {
+    {
         // Lanes over the plane's list entries: entry k (row i) goes to every tile whose window
         // holds row i, at that tile's marker index + 1 + (k - first list entry of the window);
-        // lanes over tiles write the markers.  Row i of an entry from its flat index through a
-        // float reciprocal (exact: the quotient's fraction stays >= 0.5/W from an integer).
+        // lanes over tiles write the markers.  Plane lists: row i of an entry from its flat
+        // index through a float reciprocal (exact: the quotient's fraction stays >= 0.5/W from
+        // an integer).  Row slots (FROM_ROWS): row i = the last row whose prefix is <= k (a
+        // five-step shuffle search), the entry at slot k - prefix(i) of that row.
         // Lane r < H: the first tile whose window holds row r, and the last.
         const int num = lane + P - NWR;
         const int tl_r = num < 0 ? 0 : num / TYT + 1;
@@ -422,8 +423,19 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
                 const uint32_t k = k0 + lane;
                 const bool live = k < total;
                 uint2 e = en0[q];
-                if (k0 > 0 && live) e = __ldg(lst + k);
-                const int i = live ? __float2int_rz(((float)e.y + 0.5f) * invW) : 0;
+                int i = 0;
+                if constexpr (FROM_ROWS) {
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {  // last row i < H with prefix(i) <= k
+                        const uint32_t pv_s = __shfl_sync(0xffffffffu, pre, (i + st) & 31);
+                        if (i + st < H && pv_s <= k) i += st;
+                    }
+                    const uint32_t pr = __shfl_sync(0xffffffffu, pre, i);
+                    if (live) e = __ldg(plist + ((int64_t)plane * H + i) * W + (k - pr));
+                } else {
+                    if (k0 > 0 && live) e = __ldg(lst + k);
+                    i = live ? __float2int_rz(((float)e.y + 0.5f) * invW) : 0;
+                }
                 const int tl = __shfl_sync(0xffffffffu, tl_r, i);
                 const int th = __shfl_sync(0xffffffffu, th_r, i);
                 for (int j = 0; j < span; ++j) {
@@ -436,89 +448,6 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_emit_kernel(
                 }
             }
         }
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < kPerWarp; ++q) {
-        const int ch = warp + q * kPlaneWarps;
-        if (ch >= nch) break;
-        const int plane = n * C + c0 + ch;
-        const uint2* lst = plist + (int64_t)plane * HW;
-        if constexpr (FROM_ROWS) {
-            // gather the plane's row slots into a contiguous shared list (row-major)
-            // list entry k lives in row r(k) = #{r in [1, H] : pv[r] <= k} at slot k - pv[r(k)];
-            // all loads of the plane are independent (lanes over entries)
-            uint2* buf = rowbuf_s + warp * HW;
-            const uint32_t total = __shfl_sync(0xffffffffu, pv[q], H);
-            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-                const uint32_t k = k0 + lane;
-                int r = 0;
-                for (int rr = 1; rr <= H; ++rr) r += (__shfl_sync(0xffffffffu, pv[q], rr) <= k) ? 1 : 0;
-                const uint32_t pr = __shfl_sync(0xffffffffu, pv[q], r);
-                if (k < total) buf[k] = __ldg(plist + ((int64_t)plane * H + r) * W + (k - pr));
-            }
-            __syncwarp();
-            lst = buf;
-            en0[q] = lst[lane < HW ? lane : 0];
-        }
-        // lane t: run [a, b) of the plane's list inside tile t's window; work = marker + run
-        const uint32_t a = __shfl_sync(0xffffffffu, pv[q], r0), b = __shfl_sync(0xffffffffu, pv[q], r1);
-        const uint32_t cnt_t = r1 > r0 ? b - a : 0u;
-        const uint32_t len = (lane < tiles && cnt_t > 0) ? 1u + cnt_t : 0u;  // no entry: no marker (R9)
-        uint32_t incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        const uint32_t wstart = incl - len;                       // first work item of tile t
-        const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t pos_t = lane < tiles ? start_s[lane][ch] : 0u;
-        // marker of tile t (R9): bit r set iff a nonzero row i = i_lo + r + ty*T, 0 <= ty < TY
-        const uint32_t pnext = __shfl_down_sync(0xffffffffu, pv[q], 1);
-        const unsigned rowbits = __ballot_sync(0xffffffffu, lane < H && pnext > pv[q]);
-        // = OR over tile rows ty of the R occupancy bits starting at row lo + ty*T (64-bit
-        // shifts: lo >= -P > -32; rows >= 32 do not exist)
-        unsigned mask_t = 0;
-        const uint64_t rb64 = (uint64_t)rowbits << 32;
-        for (int ty = 0; ty < TY; ++ty) {
-            const int sh = 32 + lo + ty * T;
-            if (sh < 64) mask_t |= (unsigned)(rb64 >> sh);
-        }
-        mask_t &= (1u << R) - 1u;
-        for (uint32_t w0 = 0; w0 < wtotal; w0 += 32) {
-            const uint32_t w = w0 + lane;
-            // my tile: the last t with wstart[t] <= w (tiles <= 32; wstart non-decreasing, wstart[0]
-            // = 0): binary search over the lanes' wstart, five shuffles whatever the tile count
-            int t = 0;
-#pragma unroll
-            for (int k = 16; k > 0; k >>= 1) {
-                if (k < tiles) {  // warp-uniform: steps that cannot move stay out (one tile: no search)
-                    const uint32_t ws_k = __shfl_sync(0xffffffffu, wstart, (t + k) & 31);
-                    if (t + k < tiles && ws_k <= w) t += k;
-                }
-            }
-            const uint32_t ws_t = __shfl_sync(0xffffffffu, wstart, t);
-            const uint32_t a_t = __shfl_sync(0xffffffffu, a, t);
-            const uint32_t p_t = __shfl_sync(0xffffffffu, pos_t, t);
-            const unsigned sh = __shfl_sync(0xffffffffu, shift_t, t);
-            uint2* st = reinterpret_cast<uint2*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(st_t), t));
-            const unsigned m_t = __shfl_sync(0xffffffffu, mask_t, t);
-            const uint32_t j = w - ws_t;  // 0 = marker, j >= 1: list entry a_t + j - 1
-            const uint32_t k = a_t + (j > 0 ? j - 1 : 0);
-            // entries 0..31 of the list sit in en0 (lane k holds entry k)
-            const uint2 ek = make_uint2(__shfl_sync(0xffffffffu, en0[q].x, k & 31),
-                                        __shfl_sync(0xffffffffu, en0[q].y, k & 31));
-            if (w < wtotal) {
-                if (j == 0) {
-                    st[p_t] = make_uint2((unsigned)(c0 + ch), (unsigned)NWIN + m_t);
-                } else {
-                    const uint2 e = k < 32 ? ek : lst[k];
-                    st[p_t + j] = make_uint2(e.x, e.y - sh);
-                }
-            }
-        }
-        if constexpr (FROM_ROWS) __syncwarp();
     }
 }
 
@@ -621,14 +550,9 @@ cudaError_t launch_compact_from_rows(const Geometry& g, int64_t n, uint32_t* cnt
     if (e != cudaSuccess) return e;
     const int ch = emit_chunk(g, n);
     const int chunks = (int)((g.C + ch - 1) / ch);
-    const size_t smem = sizeof(uint2) * kPlaneWarps * g.H * g.W;
     auto kern = ch == 32 ? compact_plane_emit_kernel<true, 32>
                          : (ch == 16 ? compact_plane_emit_kernel<true, 16> : compact_plane_emit_kernel<true, 8>);
-    if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    kern<<<(unsigned)(n * chunks), kPlaneWarps * 32, smem, st>>>(
+    kern<<<(unsigned)(n * chunks), kPlaneWarps * 32, 0, st>>>(
         rows, rcnt, cnt, (int)g.C, (int)g.H, (int)g.W, (int)g.ty, (int)g.T, (int)g.P, (int)g.nwr, (int)g.nwin,
         (int)g.tiles, g.cap, chunks, entries, offs, Gate{});
     return cudaGetLastError();
