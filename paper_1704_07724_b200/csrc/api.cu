@@ -22,6 +22,7 @@ struct sc_plan_s {
     DenseGeom dg;
     BwdGeom bg;
     float* bws = nullptr;      // backward: wgrad partials [splits_w][K][Cg][R][S]
+    float* bdt = nullptr;      // backward: k-contiguous copy of dout [N][G][kchunks][Ho*Wo][kc]
     float* wpack = nullptr;    // [G][Kg_pad/kbw][Cg][R][S][kbw] (pack.cu)
     float* wdense = nullptr;   // dense path A operand [G][mtiles][kblocks][128x32], TF32, swizzled
     float* nhwc = nullptr;     // dense path: channels-last TF32 copy of the input [N][H][W][Cp]
@@ -217,6 +218,7 @@ void free_plan(sc_plan_s* p) {
     if (p->ev_start) cudaEventDestroy(p->ev_start);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->bws);
+    cudaFree(p->bdt);
     delete p;
 }
 
@@ -408,7 +410,8 @@ sc_status sparse_conv_create(const sc_conv_params* params, const float* d_weight
         (e = cudaMalloc(&plan->offs, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess ||
         (e = cudaMalloc(&plan->sel, 4 * sizeof(unsigned long long))) != cudaSuccess ||
         (plan->bg.supported &&
-         (e = cudaMalloc(&plan->bws, sizeof(float) * plan->bg.splits_w * g.K * g.Cg * g.R * g.S)) != cudaSuccess) ||
+         ((e = cudaMalloc(&plan->bws, sizeof(float) * plan->bg.splits_w * g.K * g.Cg * g.R * g.S)) != cudaSuccess ||
+          (e = cudaMalloc(&plan->bdt, sizeof(float) * plan->bg.doutT_floats)) != cudaSuccess)) ||
         (sc::compact_uses_counts(g) &&
          ((e = cudaMalloc(&plan->cnt, sizeof(uint32_t) * g.N * g.tiles * g.C)) != cudaSuccess ||
           (e = cudaMalloc(&plan->plist, sizeof(uint2) * g.N * g.C * g.H * g.W)) != cudaSuccess ||
@@ -737,8 +740,8 @@ sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float* d_in, const
         plan->lists_layout = e == cudaSuccess ? 1 : 0;
     }
     if (e == cudaSuccess)
-        e = sc::launch_backward(plan->g, plan->bg, n, plan->plist, plan->prow, d_dout, plan->wpack, plan->bws, d_dw,
-                                d_dbias, d_dz, s);
+        e = sc::launch_backward(plan->g, plan->bg, n, plan->plist, plan->prow, d_dout, plan->wpack, plan->bws,
+                                plan->bdt, d_dw, d_dbias, d_dz, s);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "backward launch");
 }
 

@@ -32,12 +32,14 @@ struct DenseGeom {
 };
 
 // Backward kernels (backward.cu): KC = 32*kl output channels
-// per warp pass, kchunks per group, cblocks of 16 channels, bands of `by` output
-// rows staged in shared memory (smem bytes), image splits for wgrad / dgrad.
+// per warp pass, kchunks per group, cblocks of 16 channels; per kernel ([0] wgrad,
+// [1] dgrad) bands of `by` output rows, two band buffers of buf_floats, smem bytes;
+// image splits for wgrad / dgrad; doutT_floats of workspace for the k-contiguous dout.
 struct BwdGeom {
-    int64_t kl, kc, kchunks, cblocks, by, bands, splits_w, splits_d, tile_floats;
-    size_t smem;
-    bool bulk;  // dout tiles by one TMA bulk copy each, double buffered
+    int64_t kl, kc, kchunks, cblocks, splits_w, splits_d, doutT_floats;
+    int64_t by[2], bands[2], buf_floats[2], nbuf[2];
+    size_t smem[2];
+    bool direct;  // dgrad: one k-chunk and one band, sums stored straight to dz (no dz planes)
     bool supported;
 };
 
@@ -91,11 +93,12 @@ cudaError_t launch_select_path(const float* in, int64_t elems, unsigned long lon
                                cudaStream_t st);
 cudaError_t launch_synth_relu(float* x, int64_t elems, double rho, uint32_t seed, cudaStream_t st);
 
-// Backward (backward.cu).  ws: [splits_w][K][Cg][R][S] floats.  dw/dbias/dz nullable.
+// Backward (backward.cu).  ws: [splits_w][K][Cg][R][S] floats; doutT: b.doutT_floats
+// (rewritten by every call).  dw/dbias/dz nullable.
 void backward_geometry(const Geometry& g, BwdGeom* b);
 cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, const uint2* plist, const uint32_t* prow,
-                            const float* dout, const float* wpack, float* ws, float* dw, float* dbias, float* dz,
-                            cudaStream_t st);
+                            const float* dout, const float* wpack, float* ws, float* doutT, float* dw, float* dbias,
+                            float* dz, cudaStream_t st);
 
 // Run-time specialised stage 2 (jit.cu): a gather variant generated for the plan's
 // shape and compiled through NVRTC when no generated variant matches.
