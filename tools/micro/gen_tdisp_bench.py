@@ -12,7 +12,10 @@ Styles (same i.i.d. data as gen_scan_bench.py):
            it uses (tcgen05.ld.32x32b.x4 per tap), waits, then FMAs
   tdnm  -- as tdisp without markers: the column rides in the entry (code = pos |
            col << 8); the dispatcher masks the position
-Usage: python gen_tdisp_bench.py out.cu && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o b out.cu && ./b
+  pair  -- brx2 with the entries loaded two at a time (one LDS.128 every other
+           dispatch, selected by a parity predicate): is the entry load on the
+           dispatch chain?
+Usage: python gen_tdisp_bench.py out.cu [styles,comma,separated] && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o b out.cu && ./b
 """
 import sys
 
@@ -41,12 +44,20 @@ def case_taps(wi, j):
 def gen(style):
     a = ["{", ".reg .b64 vv, wa2, wb2;", ".reg .b32 xc, cc, xn, cn, ep, wa, col, ta, cx;",
          ".reg .b32 " + ", ".join(f"tw{i}" for i in range(24)) + ";"]
-    nreg = NACC + (NWREG if style == "brx2" else 0)
+    regw = style in ("brx2", "pair")  # weights in registers
+    nreg = NACC + (NWREG if regw else 0)
     STREAM, WBASE = nreg, nreg + 1
     labels = [f"C{i}_%=" for i in range(NPOS)] + ["LW_%=", "END_%="]
-    a += [f"mov.b32 ep, %{STREAM};", "mov.b32 col, 0;", "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
-          "LOOP_%=:", "mov.b32 xc, xn;", "mov.b32 cc, cn;", "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
-          "mov.b64 vv, {xc, xc};"]
+    if style == "pair":  # entries loaded two at a time (LDS.128 every other dispatch)
+        a += [".reg .b32 x0, c0, x1, c1, par;", ".reg .pred podd;", f"mov.b32 ep, %{STREAM};", "mov.b32 col, 0;",
+              "ld.shared.v4.b32 {x0, c0, x1, c1}, [ep];", "add.u32 ep, ep, 16;", "mov.b32 par, 0;",
+              "LOOP_%=:", "setp.ne.b32 podd, par, 0;", "selp.b32 xc, x1, x0, podd;", "selp.b32 cc, c1, c0, podd;",
+              "@podd ld.shared.v4.b32 {x0, c0, x1, c1}, [ep];", "@podd add.u32 ep, ep, 16;", "xor.b32 par, par, 1;",
+              "mov.b64 vv, {xc, xc};"]
+    else:
+        a += [f"mov.b32 ep, %{STREAM};", "mov.b32 col, 0;", "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
+              "LOOP_%=:", "mov.b32 xc, xn;", "mov.b32 cc, cn;", "ld.shared.v2.b32 {xn, cn}, [ep];",
+              "add.u32 ep, ep, 8;", "mov.b64 vv, {xc, xc};"]
     if style == "tdnm":
         a += ["and.b32 cx, cc, 255;", "TS_%=: .branchtargets " + ", ".join(labels) + ";", "brx.idx.uni cx, TS_%=;"]
     else:
@@ -55,7 +66,7 @@ def gen(style):
         wi, j = divmod(q, W)
         taps = case_taps(wi, j)
         a.append(f"C{q}_%=:")
-        if style == "brx2":
+        if regw:
             for tap, accs in taps:
                 for acc, h in accs:
                     a.append(f"fma.rn.f32x2 %{acc}, %{NACC + 2 * tap + h}, vv, %{acc};")
@@ -75,7 +86,7 @@ def gen(style):
                     a.append(f"fma.rn.f32x2 %{acc}, {'wa2' if h == 0 else 'wb2'}, vv, %{acc};")
         a.append("bra.uni LOOP_%=;")
     a.append("LW_%=:")
-    if style == "brx2":
+    if regw:
         a += ["and.b32 wa, xc, 15;", f"mad.lo.u32 wa, wa, 4608, %{WBASE};"]
         for t in range(9):
             a.append(f"ld.shared.v2.b64 {{%{NACC + 2 * t}, %{NACC + 2 * t + 1}}}, [wa+{t * 512}];")
@@ -117,7 +128,7 @@ TMEM_FREE = r"""
 def kernel(style):
     body, nreg = gen(style)
     body = body.replace("\n", "\\n").replace('"', '\\"')
-    tm = style != "brx2"
+    tm = style not in ("brx2", "pair")
     outs = ", ".join([f'"+l"(acc[{i}])' for i in range(NACC)] +
                      ([f'"+l"(w[{i}])' for i in range(NWREG)] if not tm else []))
     bounds = 512 if tm else 384
@@ -180,6 +191,7 @@ int main(int argc, char** argv) {
     }
   }
   for (int i = 0; i < 2; ++i) { ent.push_back(0); ent.push_back(NPOS + 1); enm.push_back(0); enm.push_back(NPOS + 1); }
+  while (buf.size() % 4) buf.push_back(0);
   const int off_m = (int)buf.size();
   buf.insert(buf.end(), ent.begin(), ent.end());
   const int off_n = (int)buf.size();
@@ -219,9 +231,9 @@ int main(int argc, char** argv) {
 
 
 def main():
-    styles = ["brx2", "tdisp", "tdnm"]
+    styles = sys.argv[2].split(",") if len(sys.argv) > 2 else ["brx2", "tdisp", "tdnm", "pair"]
     src = HOST.replace("%KERNELS%", "\n".join(kernel(s) for s in styles))
-    src = src.replace("%KLIST%", ", ".join(f'{{k_{s}, "{s}", {12 if s == "brx2" else 16}}}' for s in styles))
+    src = src.replace("%KLIST%", ", ".join(f'{{k_{s}, "{s}", {12 if s in ("brx2", "pair") else 16}}}' for s in styles))
     src = src.replace("%NPOS%", str(NPOS))
     open(sys.argv[1], "w").write(src)
 
