@@ -12,6 +12,10 @@ Styles (same i.i.d. data as gen_scan_bench.py):
            it uses (tcgen05.ld.32x32b.x4 per tap), waits, then FMAs
   tdnm  -- as tdisp without markers: the column rides in the entry (code = pos |
            col << 8); the dispatcher masks the position
+  solo  -- brx2 where a channel with a single entry in the window is one solo entry
+           (its case loads the taps it reaches) plus a data word with the channel,
+           instead of marker + entry
+  sdnm  -- no markers, every case loads its taps from shared memory
   pair  -- brx2 with the entries loaded two at a time (one LDS.128 every other
            dispatch, selected by a parity predicate): is the entry load on the
            dispatch chain?
@@ -44,10 +48,12 @@ def case_taps(wi, j):
 def gen(style):
     a = ["{", ".reg .b64 vv, wa2, wb2;", ".reg .b32 xc, cc, xn, cn, ep, wa, col, ta, cx;",
          ".reg .b32 " + ", ".join(f"tw{i}" for i in range(24)) + ";"]
-    regw = style in ("brx2", "pair")  # weights in registers
+    regw = style in ("brx2", "pair", "solo", "solo1")  # weights in registers
     nreg = NACC + (NWREG if regw else 0)
     STREAM, WBASE = nreg, nreg + 1
     labels = [f"C{i}_%=" for i in range(NPOS)] + ["LW_%=", "END_%="]
+    if style in ("solo", "solo1"):  # + one case per position for a channel's only entry in the window
+        labels += [f"S{i}_%=" for i in range(NPOS)]
     if style == "pair":  # entries loaded two at a time (LDS.128 every other dispatch)
         a += [".reg .b32 x0, c0, x1, c1, par;", ".reg .pred podd;", f"mov.b32 ep, %{STREAM};", "mov.b32 col, 0;",
               "ld.shared.v4.b32 {x0, c0, x1, c1}, [ep];", "add.u32 ep, ep, 16;", "mov.b32 par, 0;",
@@ -58,7 +64,7 @@ def gen(style):
         a += [f"mov.b32 ep, %{STREAM};", "mov.b32 col, 0;", "ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;",
               "LOOP_%=:", "mov.b32 xc, xn;", "mov.b32 cc, cn;", "ld.shared.v2.b32 {xn, cn}, [ep];",
               "add.u32 ep, ep, 8;", "mov.b64 vv, {xc, xc};"]
-    if style == "tdnm":
+    if style == "tdnm" or style.startswith("sdnm") or style == "solo1":
         a += ["and.b32 cx, cc, 255;", "TS_%=: .branchtargets " + ", ".join(labels) + ";", "brx.idx.uni cx, TS_%=;"]
     else:
         a += ["TS_%=: .branchtargets " + ", ".join(labels) + ";", "brx.idx.uni cc, TS_%=;"]
@@ -71,20 +77,46 @@ def gen(style):
                 for acc, h in accs:
                     a.append(f"fma.rn.f32x2 %{acc}, %{NACC + 2 * tap + h}, vv, %{acc};")
         else:
-            if style == "tdnm":
-                a += ["shr.u32 ta, cc, 8;", f"add.u32 ta, ta, %{WBASE};"]
+            if style.startswith("sdnm"):  # weights from shared memory: channel block (c % 16) * 9 taps * 512 B
+                a += ["shr.u32 ta, cc, 8;", "and.b32 ta, ta, 15;", f"mad.lo.u32 ta, ta, 4608, %{WBASE};"]
+                for i, (tap, _) in enumerate(taps):
+                    a.append(f"ld.shared.v4.b32 {{tw{4 * i}, tw{4 * i + 1}, tw{4 * i + 2}, tw{4 * i + 3}}}, [ta+{tap * 512}];")
             else:
-                a += ["mov.b32 ta, col;"]
-            for i, (tap, _) in enumerate(taps):
-                a.append(f"tcgen05.ld.sync.aligned.32x32b.x4.b32 {{tw{4 * i}, tw{4 * i + 1}, tw{4 * i + 2}, tw{4 * i + 3}}}, "
-                         f"[ta+{tap * 4}];")
-            a.append("tcgen05.wait::ld.sync.aligned;")
+                if style == "tdnm":
+                    a += ["shr.u32 ta, cc, 8;", f"add.u32 ta, ta, %{WBASE};"]
+                else:
+                    a += ["mov.b32 ta, col;"]
+                for i, (tap, _) in enumerate(taps):
+                    a.append(f"tcgen05.ld.sync.aligned.32x32b.x4.b32 {{tw{4 * i}, tw{4 * i + 1}, tw{4 * i + 2}, tw{4 * i + 3}}}, "
+                             f"[ta+{tap * 4}];")
+                a.append("tcgen05.wait::ld.sync.aligned;")
             for i, (tap, accs) in enumerate(taps):
                 a.append(f"mov.b64 wa2, {{tw{4 * i}, tw{4 * i + 1}}};")
                 a.append(f"mov.b64 wb2, {{tw{4 * i + 2}, tw{4 * i + 3}}};")
                 for acc, h in accs:
                     a.append(f"fma.rn.f32x2 %{acc}, {'wa2' if h == 0 else 'wb2'}, vv, %{acc};")
         a.append("bra.uni LOOP_%=;")
+    if style in ("solo", "solo1"):
+        # solo: entry (x, SOLO0 + q) followed by a data entry (channel, 0): the channel is the
+        # prefetched next entry; load the taps q reaches into the weight registers, skip the
+        # data entry (re-prefetch), apply the FMAs.  solo1: one entry (x, SOLO0 + q | c << 8),
+        # every dispatch masks the code
+        for q in range(NPOS):
+            wi, j = divmod(q, W)
+            taps = case_taps(wi, j)
+            a.append(f"S{q}_%=:")
+            if style == "solo":
+                a += ["and.b32 wa, xn, 15;", f"mad.lo.u32 wa, wa, 4608, %{WBASE};"]
+            else:
+                a += ["shr.u32 wa, cc, 8;", "and.b32 wa, wa, 15;", f"mad.lo.u32 wa, wa, 4608, %{WBASE};"]
+            for tap, _ in taps:
+                a.append(f"ld.shared.v2.b64 {{%{NACC + 2 * tap}, %{NACC + 2 * tap + 1}}}, [wa+{tap * 512}];")
+            if style == "solo":
+                a += ["ld.shared.v2.b32 {xn, cn}, [ep];", "add.u32 ep, ep, 8;"]
+            for tap, accs in taps:
+                for acc, h in accs:
+                    a.append(f"fma.rn.f32x2 %{acc}, %{NACC + 2 * tap + h}, vv, %{acc};")
+            a.append("bra.uni LOOP_%=;")
     a.append("LW_%=:")
     if regw:
         a += ["and.b32 wa, xc, 15;", f"mad.lo.u32 wa, wa, 4608, %{WBASE};"]
@@ -128,11 +160,12 @@ TMEM_FREE = r"""
 def kernel(style):
     body, nreg = gen(style)
     body = body.replace("\n", "\\n").replace('"', '\\"')
-    tm = style not in ("brx2", "pair")
+    regw = style in ("brx2", "pair", "solo", "solo1")
+    tm = style in ("tdisp", "tdnm")
     outs = ", ".join([f'"+l"(acc[{i}])' for i in range(NACC)] +
-                     ([f'"+l"(w[{i}])' for i in range(NWREG)] if not tm else []))
-    bounds = 512 if tm else 384
-    wdecl = "" if tm else f"unsigned long long w[{NWREG}]; for (int i = 0; i < {NWREG}; ++i) w[i] = 0ull;"
+                     ([f'"+l"(w[{i}])' for i in range(NWREG)] if regw else []))
+    bounds = 384 if (regw or style == "sdnm12") else 512
+    wdecl = f"unsigned long long w[{NWREG}]; for (int i = 0; i < {NWREG}; ++i) w[i] = 0ull;" if regw else ""
     return f'''
 extern "C" __global__ void __launch_bounds__({bounds}, 1) k_{style}(const unsigned* __restrict__ g_buf, int nwords,
     int soff, float* out, int nwarps, int reps) {{
@@ -176,26 +209,46 @@ int main(int argc, char** argv) {
   std::uniform_real_distribution<float> U(0.f, 1.f);
   std::vector<unsigned> buf(16 * 9 * 128);   // weights: 16 channels x 9 taps x 128 floats
   for (auto& x : buf) { float f = 1e-3f * U(rng); x = *reinterpret_cast<unsigned*>(&f); }
-  std::vector<unsigned> ent, enm;   // with markers / without (column in the code)
+  std::vector<unsigned> ent, enm, ens;   // with markers / without (TMEM column / channel in the code)
   long nnz = 0, fmas = 0;
   auto nf = [&](int q) { int wi = q / W, j = q % W, c = 0; for (int ty = 0; ty < 2; ++ty) { int r = wi - ty; if (r < 0 || r > 2) continue;
       for (int x = 0; x < W; ++x) { int t = j + 1 - x; if (t >= 0 && t < 3) c += 2; } } return c; };
+  std::vector<unsigned> eso, es1;   // solo forms: a channel with one entry -> (x, SOLO0 + q), (c, 0) / (x, SOLO0 + q | c << 8)
   for (int c = 0; c < nch; ++c) {
     int k = 0;
+    std::vector<unsigned> cq, cb;
     for (int q = 0; q < NPOS; ++q) if (U(rng) < rho) {
+      { float f0 = 0; (void)f0; }
       float f = 1.0f + U(rng); unsigned b = *reinterpret_cast<unsigned*>(&f);
       if (k == 0) { ent.push_back((unsigned)c); ent.push_back((unsigned)NPOS); }
       ent.push_back(b); ent.push_back((unsigned)q);
       enm.push_back(b); enm.push_back((unsigned)q | ((unsigned)((c % 14) * 36) << 8));
+      ens.push_back(b); ens.push_back((unsigned)q | ((unsigned)(c % 16) << 8));
+      cq.push_back((unsigned)q); cb.push_back(b);
       ++nnz; fmas += nf(q); ++k;
     }
+    if (cq.size() == 1) { eso.push_back(cb[0]); eso.push_back((unsigned)(NPOS + 2) + cq[0]); eso.push_back((unsigned)c); eso.push_back(0u);
+                          es1.push_back(cb[0]); es1.push_back(((unsigned)(NPOS + 2) + cq[0]) | ((unsigned)(c % 16) << 8)); }
+    else if (cq.size() > 1) {
+      eso.push_back((unsigned)c); eso.push_back((unsigned)NPOS);
+      es1.push_back((unsigned)c); es1.push_back((unsigned)NPOS);
+      for (size_t i = 0; i < cq.size(); ++i) { eso.push_back(cb[i]); eso.push_back(cq[i]); es1.push_back(cb[i]); es1.push_back(cq[i]); }
+    }
   }
-  for (int i = 0; i < 2; ++i) { ent.push_back(0); ent.push_back(NPOS + 1); enm.push_back(0); enm.push_back(NPOS + 1); }
+  for (int i = 0; i < 2; ++i) { eso.push_back(0); eso.push_back(NPOS + 1); es1.push_back(0); es1.push_back(NPOS + 1); }
+  for (int i = 0; i < 2; ++i) { ent.push_back(0); ent.push_back(NPOS + 1); enm.push_back(0); enm.push_back(NPOS + 1);
+                                ens.push_back(0); ens.push_back(NPOS + 1); }
   while (buf.size() % 4) buf.push_back(0);
   const int off_m = (int)buf.size();
   buf.insert(buf.end(), ent.begin(), ent.end());
   const int off_n = (int)buf.size();
   buf.insert(buf.end(), enm.begin(), enm.end());
+  const int off_s = (int)buf.size();
+  buf.insert(buf.end(), ens.begin(), ens.end());
+  const int off_o = (int)buf.size();
+  buf.insert(buf.end(), eso.begin(), eso.end());
+  const int off_1 = (int)buf.size();
+  buf.insert(buf.end(), es1.begin(), es1.end());
   const int nwords = (int)buf.size();
   unsigned* d; float* o;
   cudaMalloc(&d, nwords * 4); cudaMalloc(&o, 148 * 512 * 4);
@@ -210,7 +263,7 @@ int main(int argc, char** argv) {
     cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, k.k);
     for (int nw : {4, 8, 11, 12, 14, 15, 16}) {
       if (nw > k.maxw) continue;
-      const int so = !strcmp(k.name, "tdnm") ? off_n : off_m;
+      const int so = !strcmp(k.name, "solo1") ? off_1 : !strcmp(k.name, "solo") ? off_o : (!strcmp(k.name, "tdnm") || !strncmp(k.name, "sdnm", 4)) ? (strncmp(k.name, "sdnm", 4) ? off_n : off_s) : off_m;
       k.k<<<148, nw * 32, nwords * 4>>>(d, nwords, so, o, nw, 1);
       cudaEventRecord(e0);
       k.k<<<148, nw * 32, nwords * 4>>>(d, nwords, so, o, nw, reps);
@@ -233,7 +286,7 @@ int main(int argc, char** argv) {
 def main():
     styles = sys.argv[2].split(",") if len(sys.argv) > 2 else ["brx2", "tdisp", "tdnm", "pair"]
     src = HOST.replace("%KERNELS%", "\n".join(kernel(s) for s in styles))
-    src = src.replace("%KLIST%", ", ".join(f'{{k_{s}, "{s}", {12 if s in ("brx2", "pair") else 16}}}' for s in styles))
+    src = src.replace("%KLIST%", ", ".join(f'{{k_{s}, "{s}", {12 if s in ("brx2", "pair", "sdnm12", "solo", "solo1") else 16}}}' for s in styles))
     src = src.replace("%NPOS%", str(NPOS))
     open(sys.argv[1], "w").write(src)
 
