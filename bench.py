@@ -510,6 +510,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(v["ms_per_step"], 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(shp, s_head, n), "global_batch": n * ws, "parallelism": f"dp{ws}",
+                   **shared_gpu_note(ws),
                    "l2": f"{v['nsets']} rotating input/output sets ({v['set_mib']:.0f} MiB > 2x L2)",
                    "timing": "CUDA events around K CUDA-graph replays (one sparse_conv_forward each), max over ranks",
                    "realized_sparsity": round(v["realized_s"], 5), "variant": vname},
@@ -655,7 +656,8 @@ def run_chain(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"c5 chain conv3->conv4->conv5, N={n_total} total ({n}/GPU), first input s={s_first}",
-                   "global_batch": n_total, "parallelism": f"dp{ws}", "l2": "inputs larger than L2 (177 MB/GPU at N=1)",
+                   "global_batch": n_total, "parallelism": f"dp{ws}", **shared_gpu_note(ws),
+                   "l2": "inputs larger than L2 (177 MB/GPU at N=1)",
                    "timing": "CUDA events around K graph replays of sparse_conv_forward_chain (intermediate layers "
                              "emit the next layer's stage-1 lists, no dense intermediates), max over ranks",
                    "layer_input_sparsity": [round(1 - c[2] / (n * shp.c * shp.h * shp.w), 4)
@@ -744,7 +746,7 @@ def run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C4 = C4a + C4b on two streams: {workload_name(shps[0], s, n)}; "
                                f"{workload_name(shps[1], s, n)}",
-                   "global_batch": n * ws, "parallelism": f"dp{ws}",
+                   "global_batch": n * ws, "parallelism": f"dp{ws}", **shared_gpu_note(ws),
                    "l2": f"{nsets} rotating input/output sets ({nsets * per_set / 2 ** 20:.0f} MiB > 2x L2)",
                    "timing": "CUDA events around K graph replays (both layers forked onto two streams), max over ranks",
                    "variants": [c.variant[1] for c in convs]},
@@ -878,6 +880,16 @@ def run_backward(args):
                       "note": "sparse_conv_backward (dw, dbias, ReLU-masked dz) graph-timed, L2-warm; cudnn_* = "
                               "torch conv2d forward+backward (dw, db, dx) per step, context only"}), flush=True)
     return 0
+
+
+def shared_gpu_note(ws):
+    """config entries of a run whose ranks share GPUs (SC_DIST_BACKEND=gloo, shard.shares_gpus)."""
+    import torch
+    if ws > 1 and shard.shares_gpus():
+        return {"functional_only": f"{ws} ranks on {torch.cuda.device_count()} GPU(s) over gloo: a check of the "
+                                   "multi-rank path (launch, process group, shard, barriers, max over ranks), "
+                                   "not a scaling measurement"}
+    return {}
 
 
 def relaunch_under_torchrun(args):

@@ -36,15 +36,28 @@ def image_start(set_index, rank, ws, n_per_rank):
     return (set_index * ws + rank) * n_per_rank
 
 
-def init(ws, local, backend="nccl"):
-    """Bind this process to its GPU and, for ws > 1, join the process group."""
+def shares_gpus():
+    """SC_DIST_BACKEND=gloo: a functional check of the multi-rank path on a box with fewer GPUs
+    than ranks -- ranks share GPUs round-robin and synchronise over gloo on the host (their
+    kernels never wait on one another: no collective on the data path).  Not a scaling number."""
+    return os.environ.get("SC_DIST_BACKEND", "nccl") == "gloo"
+
+
+def init(ws, local, backend=None):
+    """Bind this process to its GPU and, for ws > 1, join the process group (NCCL, one GPU
+    per rank; gloo with GPUs shared round-robin when SC_DIST_BACKEND=gloo)."""
     import torch
+    gloo = shares_gpus() if backend is None else backend == "gloo"
+    idx = local % max(1, torch.cuda.device_count()) if gloo else local
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(idx)
         if not dist.is_initialized():
-            dist.init_process_group(backend, device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if ws > 1 else 0)
+            if gloo:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", idx))
+    dev = torch.device("cuda", idx if ws > 1 else 0)
     torch.cuda.set_device(dev)
     return dev
 
@@ -60,6 +73,8 @@ def _reduce(value, ws, device, op):
         return float(value)
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        device = None  # host tensors (gloo)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=op)
     return float(t.item())

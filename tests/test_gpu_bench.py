@@ -56,3 +56,23 @@ def test_bench_chain_config_strong_scaling_line():
     d = run_bench("--config", "C5", "--gpus", "1", "--steps", "1", "--warmup", "3", "--no-cpu-baseline")
     assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["config"]["global_batch"] == 1024
     assert len(d["layers_unfused_us"]) == 3 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("config,batch", [("C2", 256), ("C5", 1024)])
+def test_two_ranks_on_one_gpu_functional(config, batch):
+    """The multi-rank path on hardware with fewer GPUs than ranks (this pool: one): `--gpus 2`
+    re-launches under torchrun, the ranks share the GPU and synchronise over gloo
+    (SC_DIST_BACKEND=gloo; their kernels never wait on one another), shard the batch
+    (C2: weak, each rank its own 128 images; C5: the 1024 images split), time between
+    barriers and take the max over ranks.  The line says it is not a scaling number."""
+    env = dict(os.environ, SC_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--gpus", "2",
+                        "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-sweep"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_batch"] == batch
+    assert "functional_only" in d["config"]
+
