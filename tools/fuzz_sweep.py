@@ -3,7 +3,7 @@ tests/test_gpu_fuzz.py -- more seeds, larger channel and filter counts, batches
 that make multi-wave stage-2 grids -- each checked like the fuzz test: stage-1
 lists bit-exact against the oracle, streams against the test-side adapter,
 sparse outputs within 1e-5*mass + 1e-6, integer data bit-exact.
-Usage: python tools/fuzz_sweep.py [seeds] [shapes per seed]"""
+Usage: python tools/fuzz_sweep.py [seeds] [shapes per seed] [first seed]"""
 import os
 import sys
 
@@ -61,9 +61,10 @@ def check(shp, sparsity):
 def main():
     seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     count = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    first = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # first seed
     fails = 0
     total = 0
-    for seed in range(seeds):
+    for seed in range(first, first + seeds):
         for shp in shapes(seed, count):
             for s in (0.95, 0.5):
                 total += 1
