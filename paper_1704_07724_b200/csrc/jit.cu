@@ -187,12 +187,17 @@ std::string gen_variant(const Params& p, const std::string& sname, const std::st
             for (size_t i = 0; i < wkeys.size(); ++i) {
                 const int r = wkeys[i].first, t = wkeys[i].second;
                 if (!((m >> r) & 1)) continue;
-                if (NPAIR == 1)
-                    asm_.push_back("ld.shared.b64 " + op(wp[key3(r, t, 0)]) + ", [ea+" +
-                                   std::to_string(i * tap_bytes) + "];");
-                else
-                    asm_.push_back("ld.shared.v2.b64 {" + op(wp[key3(r, t, 0)]) + ", " + op(wp[key3(r, t, 1)]) +
-                                   "}, [ea+" + std::to_string(i * tap_bytes) + "];");
+                // pairs (k0,k1),(k2,k3) per 16-byte load when the lane stride (8*NPAIR bytes) keeps
+                // them 16-byte aligned (NPAIR even), else one 8-byte load per pair (KL = 6)
+                const int step = NPAIR % 2 == 0 ? 2 : 1;
+                for (int pi = 0; pi < NPAIR; pi += step) {
+                    const std::string off = std::to_string(i * tap_bytes + 8 * pi);
+                    if (step == 2)
+                        asm_.push_back("ld.shared.v2.b64 {" + op(wp[key3(r, t, pi)]) + ", " +
+                                       op(wp[key3(r, t, pi + 1)]) + "}, [ea+" + off + "];");
+                    else
+                        asm_.push_back("ld.shared.b64 " + op(wp[key3(r, t, pi)]) + ", [ea+" + off + "];");
+                }
                 if (NSING)
                     asm_.push_back("ld.shared.f32 " + op(ws[key3(r, t, 0)]) + ", [es+" +
                                    std::to_string(i * tap_bytes + 256) + "];");

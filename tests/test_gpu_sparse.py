@@ -131,6 +131,54 @@ def test_integer_data_bitexact_table2(sc):
         assert np.array_equal(out.astype(np.float64), ref), shp.name
 
 
+# Stage-2 kernel a plan picks for the 1x1 Table 2 layers (tools/gen_gather.py VARIANTS: the
+# wide k-block tilings V53/V54/V55 need Kg >= KMIN, else the round-1 V43/V45).
+T2_1X1_VARIANT = {"GoogLeNet-Inception4a.1": 53, "GoogLeNet-Inception4a.2": 43, "GoogLeNet-Inception5a.1": 54,
+                  "GoogLeNet-Inception5a.2": 55}
+
+
+def test_table2_1x1_variant_choice(sc):
+    for shp, _ in datagen.table2_shapes(n=2):
+        if shp.name in T2_1X1_VARIANT:
+            w, b = datagen.weights(shp)
+            assert make_conv(sc, shp, w, b).variant[0] == T2_1X1_VARIANT[shp.name], shp.name
+
+
+@pytest.mark.parametrize("k,wd,groups,want", [(151, 14, 1, 53), (149, 14, 1, 43), (201, 7, 1, 54), (199, 7, 1, 55),
+                                                (150, 7, 1, 55), (149, 7, 1, 45), (300, 7, 1, 54), (402, 7, 2, 54)])
+def test_wide_kblock_1x1_ragged(sc, k, wd, groups, want):
+    """KL = 6 / 8 tiles (k-blocks of 192 / 256 channels) at the KMIN edges and with ragged
+    last k-blocks (zero-padded weights, pack.cu) and groups: tolerance at s=0.9 on all
+    outputs, stage-1 lists bit-exact, integer data bit-exact."""
+    shp = datagen.ConvShape(f"wide_kblock_{k}_{wd}_{groups}", 5000 + k + wd, 3, 38 * groups, wd, wd, k, 1, 1, 1, 0,
+                            groups)
+    x = datagen.activations(shp, 0.9, seed=k)
+    w, b = datagen.weights(shp, seed=k)
+    conv = make_conv(sc, shp, w, b, max_batch=4)
+    assert conv.variant[0] == want
+    out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    check_lists(conv, x, 3)
+    check_conv(out, x, w, b, shp)
+    xi, wi, bi = datagen.integer_case(shp, sparsity=0.7)
+    conv = make_conv(sc, shp, wi, bi, max_batch=4)
+    out = conv.forward(torch.from_numpy(xi).to(DEV)).cpu().numpy()
+    ref, _ = oracle.conv_fp64(xi, wi, bi, shp.stride, shp.pad, shp.groups)
+    assert np.array_equal(out.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("layer,variant", [("GoogLeNet-Inception4a.1", 48), ("GoogLeNet-Inception5a.1", 49)])
+def test_superseded_t2_tilings(sc, layer, variant, monkeypatch):
+    """The round-1 1x1 tilings V48 / V49 (no longer built in), generated at run time."""
+    want = force_kernel(monkeypatch, variant)
+    shp = {t.name: t for t, _ in datagen.table2_shapes(n=2)}[layer]
+    x = datagen.activations(shp, 0.9, seed=5)
+    w, b = datagen.weights(shp, seed=5)
+    conv = make_conv(sc, shp, w, b)
+    assert conv.variant[0] == want
+    out = conv.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    check_conv(out, x, w, b, shp)
+
+
 @pytest.mark.parametrize("cfg", ["C2", "C3", "C4b"])
 def test_zero_input_gives_bias(sc, cfg):
     shp = datagen.CONFIGS[cfg].with_batch(2)
@@ -295,7 +343,7 @@ JIT_TILINGS = {1: "7,2,7,1,8,4,3,254", 2: "3,2,7,1,8,4,3,254", 3: "2,2,7,1,4,4,3
                5: "6,2,7,1,4,4,3,254", 28: "1,4,11,1,16,2,3,254", 29: "4,1,11,1,16,2,3,254",
                7: "7,1,11,1,16,4,3,254", 10: "3,3,11,1,8,4,3,254", 11: "3,4,7,1,8,3,3,254",
                12: "2,4,11,1,8,3,3,254", 13: "5,2,11,1,8,4,3,254", 14: "1,4,11,1,8,3,3,254",
-               30: "2,1,11,1,16,2,3,254"}
+               30: "2,1,11,1,16,2,3,254", 48: "3,3,11,1,16,2,2,254", 49: "2,4,11,1,16,3,3,510"}
 FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28, 51)] +
           [("C4b", v) for v in (0, 4, 29, 30, 52)] + [("C3", v) for v in (0, 3, 33)] + [("C1", v) for v in (0, 5, 50)])
 

@@ -52,13 +52,17 @@ VARIANTS = [
     (40, "r5s5p1t2_w11_ty2_kl2_sl2p126", 5, 5, 1, 11, 2, 2, 11, 1, 16, 2, None, 2, 126, 2),  # LeNet-Conv2 (T=2)
     (41, "r5s5p2_w6_ty1_kl1_s3sl2p126", 5, 5, 2, 6, 1, 1, 11, 1, 16, 3, None, 2, 126),     # AlexNetC-Conv3
     (42, "r3s3p1_w5_ty3_kl2_sl2", 3, 3, 1, 5, 3, 2, 11, 1, 16, 2, None, 2, 254),           # AlexNetI-Conv4
-    (48, "r1s1p0_w14_ty3_kl3_sl2_k150", 1, 1, 0, 14, 3, 3, 11, 1, 16, 2, None, 2, 254, 1, 150),  # Inception4a.1
     (43, "r1s1p0_w14_ty2_kl4", 1, 1, 0, 14, 2, 4, 11, 1, 32, 2),                           # Inception4a.2
     (44, "r3s3p1_w14_ty3_kl2_s3sl2", 3, 3, 1, 14, 3, 2, 11, 1, 16, 3, None, 2, 254),       # Inception4e.3
-    (49, "r1s1p0_w7_ty2_kl4_s3p510_k200", 1, 1, 0, 7, 2, 4, 11, 1, 16, 3, None, 3, 510, 1, 200),  # Inception5a.1
     (45, "r1s1p0_w7_ty2_kl2_sl2", 1, 1, 0, 7, 2, 2, 11, 1, 16, 2, None, 2, 254),           # Inception5a.2
     (46, "r3s3p1_w7_ty2_kl4_p126", 3, 3, 1, 7, 2, 4, 11, 1, 16, 2, None, 3, 126),          # Inception5b.3
     (47, "r5s5p2_w7_ty2_kl2_sl2p126", 5, 5, 2, 7, 2, 2, 11, 1, 16, 2, None, 2, 126),       # Inception5b.5
+    # round 2: 1x1 layers with one dispatch per nonzero for all of a k-block of 32*KL >= Kg
+    # channels (KL = 6, 8; no halo, so the tile height buys no reuse: TY = 1), 32-channel
+    # weight chunks (profiles/r2_t2_kl68_tune.txt), replacing V48 / V49
+    (53, "r1s1p0_w14_ty1_kl6_ch32sl2_k150", 1, 1, 0, 14, 1, 6, 11, 1, 32, 2, None, 2, 254, 1, 150),  # Inception4a.1
+    (54, "r1s1p0_w7_ty1_kl8_ch32s3_k200", 1, 1, 0, 7, 1, 8, 11, 1, 32, 3, None, 3, 254, 1, 200),     # Inception5a.1
+    (55, "r1s1p0_w7_ty1_kl6_ch32s3sl2p510_k150", 1, 1, 0, 7, 1, 6, 11, 1, 32, 3, None, 2, 510, 1, 150),  # Inception5a.2
 ]
 
 # Superseded round-1 tilings (slower than the shipped variant of the same shape, DESIGN.md
@@ -66,6 +70,8 @@ VARIANTS = [
 # into libsparseconv.so; any of them can be generated at run time for tuning or tests with
 # SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE" (csrc/jit.cu).
 SUPERSEDED = [
+    (48, "r1s1p0_w14_ty3_kl3_sl2_k150", 1, 1, 0, 14, 3, 3, 11, 1, 16, 2, None, 2, 254, 1, 150),  # Inception4a.1 until round 2
+    (49, "r1s1p0_w7_ty2_kl4_s3p510_k200", 1, 1, 0, 7, 2, 4, 11, 1, 16, 3, None, 3, 510, 1, 200),  # Inception5a.1 until round 2
     (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 until round 2
     (28, "r3s3p1_w28_ty1_kl4_nw11_ch16s2", 3, 3, 1, 28, 1, 4, 11, 1, 16, 2),   # C4a until round 2
     (29, "r5s5p2_w28_ty4_kl1_nw11", 5, 5, 2, 28, 4, 1, 11, 1, 16, 2),        # C4b until round 2
@@ -87,7 +93,7 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 51, 52, 33, 50, 48, 49]  # 48/49 need Kg >= KMIN
+PRIORITY = [21, 51, 52, 33, 50, 53, 54, 55]  # 53/54/55 need Kg >= KMIN (54 before 55)
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):
@@ -269,10 +275,16 @@ def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None
             for i, key in enumerate(wkeys):
                 if key[0] not in rows:
                     continue
-                if NPAIR == 1:
-                    asm.append(f"ld.shared.b64 %{wp[(key, 0)]}, [ea+{i * tap_bytes}];")
-                else:
-                    asm.append(f"ld.shared.v2.b64 {{%{wp[(key, 0)]}, %{wp[(key, 1)]}}}, [ea+{i * tap_bytes}];")
+                # the lane's KL weights of a tap (lane-contiguous, 8*NPAIR bytes per lane, pack.cu):
+                # pairs (k0,k1),(k2,k3) per 16-byte load when the lane stride keeps them 16-byte
+                # aligned (NPAIR even), else one 8-byte load per pair (KL = 6)
+                step = 2 if NPAIR % 2 == 0 else 1
+                for pi in range(0, NPAIR, step):
+                    off = i * tap_bytes + 8 * pi
+                    if step == 2:
+                        asm.append(f"ld.shared.v2.b64 {{%{wp[(key, pi)]}, %{wp[(key, pi + 1)]}}}, [ea+{off}];")
+                    else:
+                        asm.append(f"ld.shared.b64 %{wp[(key, pi)]}, [ea+{off}];")
                 if NSING:
                     asm.append(f"ld.shared.f32 %{ws[key]}, [es+{i * tap_bytes + 256}];")
         asm.append("bra.uni LOOP_%=;")

@@ -36,8 +36,11 @@ def main():
     vid = sys.argv[1] if sys.argv[1].startswith("jit:") else int(sys.argv[1])
     cfg = sys.argv[2] if len(sys.argv) > 2 else "C2"
     sps = [float(v) for v in sys.argv[3:]] or [0.9, 0.95, 0.99]
-    cfg, _, nimg = cfg.partition(":")   # "C2:512" overrides the batch
-    shp = datagen.CONFIGS[cfg]
+    cfg, _, nimg = cfg.partition(":")   # "C2:512" overrides the batch; "T2.<layer>" = a paper Table 2 layer
+    if cfg.startswith("T2."):
+        shp = {s.name: s for s, _ in datagen.table2_shapes(128)}[cfg[3:]]
+    else:
+        shp = datagen.CONFIGS[cfg]
     if nimg:
         shp = dataclasses.replace(shp, n=int(nimg))
     wn, bn = datagen.weights(shp)
