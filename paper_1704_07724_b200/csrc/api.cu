@@ -108,7 +108,8 @@ void stream_format(Geometry* g, int64_t ty) {
 // env: never generate at run time) and fix what it implies: packed-weight k-block
 // width and the stream row tiles.  No generated variant matches -> a run-time
 // generated one (variant -1, parameters in *jp) if allow_jit and the shape is in range.
-void choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit, sc::jit::Params* jp) {
+// Returns why an SC_JIT_FORCE parameter set cannot run this shape (nullptr: chosen fine).
+const char* choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit, sc::jit::Params* jp) {
     int force = -1;
     if (const char* f = getenv("SC_FORCE_VARIANT")) force = atoi(f);
     int kl = 1, ty = (int)g->Ho;
@@ -121,6 +122,7 @@ void choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit,
             if (sscanf(jf, "%d,%d,%d,%d,%d,%d,%d,%d", &q.TY, &q.KL, &q.NW, &q.MINB, &q.CH, &q.STAGES, &q.SLOTS,
                        &q.PIECE) == 8) {
                 q.R = (int)g->R; q.S = (int)g->S; q.P = (int)g->P; q.T = (int)g->T; q.W = (int)g->W;
+                if (const char* why = sc::jit::invalid(*g, q)) return why;
                 *jp = q;
                 *variant = -1;
                 *name = "jit";
@@ -141,6 +143,7 @@ void choose_kernel(Geometry* g, int* variant, const char** name, bool allow_jit,
     g->Kg_pad = (g->Kg + g->kbw - 1) / g->kbw * g->kbw;
     g->kblocks = g->Kg_pad / g->kbw;
     stream_format(g, ty);
+    return nullptr;
 }
 
 sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int* variant, const char** name,
@@ -153,7 +156,8 @@ sc_status make_geometry(const sc_conv_params* p, Geometry* g, DenseGeom* dg, int
     g->Kg = p->k / p->groups;
     g->relu = (p->flags & SC_FLAG_FUSE_RELU) != 0;
     sc::jit::Params unused;
-    choose_kernel(g, variant, name, allow_jit && jp, jp ? jp : &unused);
+    if (const char* why = choose_kernel(g, variant, name, allow_jit && jp, jp ? jp : &unused))
+        return fail(SC_ERR_UNSUPPORTED, "SC_JIT_FORCE=%s: %s", getenv("SC_JIT_FORCE"), why);
     sc::dense_geometry(*g, dg);
     const int64_t in_e = g->N * g->C * g->H * g->W, out_e = g->N * g->K * g->Ho * g->Wo;
     const int64_t w_e = g->G * g->Cg * g->R * g->S * g->Kg_pad;

@@ -8,7 +8,7 @@ namespace fast {
 template <class V>
 bool matches(const Geometry& g) {
     return g.T == V::T && g.R == V::R && g.S == V::S && g.P == V::P && g.W == V::W && g.Wo == V::WO && g.Cg >= 1 &&
-           (g.Cg + V::CH - 1) / V::CH <= 63 && g.Kg >= V::KMIN;
+           (g.Cg + V::CH - 1) / V::CH <= 63 && g.Kg >= V::KMIN && (V::KMIN == 0 || V::KL == wide_1x1_kl(g));
 }
 #define SC_DECLARE(VV)                                                                                  \
     cudaError_t launch_##VV(const Geometry& g, int64_t n, const uint2* entries, const uint32_t* offs,   \

@@ -270,6 +270,22 @@ static bool epilogue_fits(const Params& p) {
     return 32 * ((er * WO) | 1) <= piece_floats;
 }
 
+const char* invalid(const Geometry& g, const Params& p) {
+    if (p.R != g.R || p.S != g.S || p.P != g.P || p.T != g.T || p.W != g.W) return "parameters of another shape";
+    if (g.R > 7 || g.S > 7 || g.W > 64 || g.T > 3) return "shape outside the generator (R, S <= 7, W <= 64, stride <= 3)";
+    if (p.KL != 1 && p.KL != 2 && p.KL != 3 && p.KL != 4 && p.KL != 6 && p.KL != 8)
+        return "KL must be 1, 2, 3, 4, 6 or 8 (the weight packings of pack.cu)";
+    if (p.KL == 1 && (p.T != 1 || p.S < 2)) return "x-pair tiles (KL = 1) need stride 1 and S >= 2";
+    if (p.TY < 1 || p.TY > g.Ho) return "TY outside [1, Ho]";
+    const int nwr = (p.TY - 1) * p.T + p.R;
+    if (nwr > 31 || nwr * p.W > 2048) return "tile window beyond the jump-table / marker-mask limits";
+    if (p.CH < 1 || (g.Cg + p.CH - 1) / p.CH > 63) return "more than 63 weight chunks (raise CH)";
+    if (p.NW < 1 || p.STAGES < 1 || p.SLOTS < 1 || p.PIECE < 2) return "NW, STAGES, SLOTS >= 1 and PIECE >= 2";
+    if (smem_bytes(p) > 220 * 1024) return "shared memory above 220 KB";
+    if (!epilogue_fits(p)) return "epilogue does not fit the piece slots (raise SLOTS or PIECE)";
+    return nullptr;
+}
+
 bool choose(const Geometry& g, Params* p) {
     *p = Params{};
     if (g.R > 7 || g.S > 7 || g.W > 64 || g.T > 3) return false;
@@ -278,6 +294,9 @@ bool choose(const Geometry& g, Params* p) {
     // k-slots per lane: four when there are enough filters, x-pairs (KL=1) for few filters at stride 1
     int kl = g.Kg > 96 ? 4 : (g.Kg > 32 ? 2 : 1);
     if (kl == 1 && (g.T != 1 || g.S < 2)) kl = 2;
+    // 1x1 at stride 1 with many filters: one-row tiles of the fewest k-blocks (sc_internal.h)
+    const bool wide = wide_1x1_kl(g) != 0;
+    if (wide) kl = wide_1x1_kl(g);
     p->KL = kl;
     const int nx = kl == 1 ? (WO + 1) / 2 : WO;
     const int acc_row = kl == 1 ? 2 * nx : nx * kl;           // registers per tile row
@@ -286,6 +305,7 @@ bool choose(const Geometry& g, Params* p) {
     int ty = (budget - wregs) / acc_row;
     if (ty < 1) return false;
     if (ty > (int)g.Ho) ty = (int)g.Ho;
+    if (wide && kl > 4) ty = 1;
     // rebalance: the same number of tiles with the smallest tile height
     const int tiles = ((int)g.Ho + ty - 1) / ty;
     ty = ((int)g.Ho + tiles - 1) / tiles;
@@ -296,11 +316,12 @@ bool choose(const Geometry& g, Params* p) {
     // the epilogue reuses the warp's piece slots: wide rows need more of them
     while (!epilogue_fits(*p) && p->SLOTS < 8) ++p->SLOTS;
     p->CH = 16;
+    if (wide && kl > 4) { p->CH = 32; p->STAGES = 3; p->SLOTS = 2; }  // V54/V55 ring
+    while (!epilogue_fits(*p) && p->SLOTS < 8) ++p->SLOTS;
     while (p->CH > 1 && smem_bytes(*p) > 200 * 1024) p->CH /= 2;
     if ((g.Cg + p->CH - 1) / p->CH > 63) p->CH = (int)((g.Cg + 62) / 63);
-    if (smem_bytes(*p) > 220 * 1024 || !epilogue_fits(*p)) return false;
     p->id = 1000;
-    return true;
+    return invalid(g, *p) == nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -470,7 +491,7 @@ size_t variant_source(const Params& p, char* buf, size_t cap) {
 cudaError_t launch(void* fn, size_t smem, const Params& p, const Geometry& g, int64_t n, const uint2* entries,
                    const uint32_t* offs, const float* wpack, const float* bias, float* out, cudaStream_t st,
                    Gate gate) {
-    if (!fn || g.ty != p.TY) return cudaErrorInvalidValue;
+    if (!fn || g.ty != p.TY || invalid(g, p)) return cudaErrorInvalidValue;
     fast::ArgsGated ag;
     fast::Args& a = ag;
     a.entries = entries; a.offs = offs; a.wpack = wpack; a.bias = bias; a.out = out;

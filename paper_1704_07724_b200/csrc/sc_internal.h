@@ -23,6 +23,20 @@ struct Geometry {
     bool relu;
 };
 
+// 1x1 convolutions at stride 1 with Kg >= 150 filters: no
+// halo, so one-row tiles, and a nonzero costs one interpreter dispatch per k-block of 32*KL
+// filters -- KL = the fewest k-blocks among 4, 6, 8 (ties to the narrower) whose one-row tile
+// (Wo*KL accumulators + KL weights) fits V21's 140 registers.  0: not such a layer.  Both the
+// shipped variants V53-V56 (gather_fast.cu) and run-time generated tilings (jit.cu) follow it.
+inline int wide_1x1_kl(const Geometry& g) {
+    if (g.R != 1 || g.S != 1 || g.T != 1 || g.Kg < 150) return 0;
+    auto blocks = [&](int64_t k) { return (g.Kg + 32 * k - 1) / (32 * k); };
+    int kl = 4;
+    for (int k : {6, 8})
+        if (blocks(k) < blocks(kl) && g.Wo * k + k <= 140) kl = k;
+    return kl;
+}
+
 // Dense tcgen05 path geometry (dense_tc.cu): channels-last input with Cp = G*Cgp
 // channels (each group's Cg padded to a multiple of 4); K-dim blocks of 32 channels per tap (cb per group); tiles
 // of `rows` whole output rows (npix = rows*Wo pixels, UMMA N = nmma).
@@ -109,6 +123,9 @@ struct Params {
 };
 bool available();                                 // NVRTC and the driver entry points are loadable
 bool choose(const Geometry& g, Params* p);       // false: shape outside the generator's limits
+// Why parameter set p cannot run shape g (nullptr: it can): generator, stream-format and
+// kernel limits (checked for SC_JIT_FORCE sets and again at launch).
+const char* invalid(const Geometry& g, const Params& p);
 // Compile (cached per parameter set and device) the ungated and the gated kernel.
 cudaError_t compile(const Params& p, int device, void** fn, void** fn_gated, size_t* smem);
 cudaError_t launch(void* fn, size_t smem, const Params& p, const Geometry& g, int64_t n, const uint2* entries,

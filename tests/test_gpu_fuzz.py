@@ -184,7 +184,14 @@ JIT_SHAPES = [  # no shipped variant: the plan generates one at creation (csrc/j
     datagen.ConvShape("jit_1x1_w17", 983, 2, 40, 17, 17, 128, 1, 1, 1, 0, 1),
     datagen.ConvShape("jit_xpair_w12", 984, 3, 8, 10, 12, 20, 3, 5, 1, 2, 2),
     datagen.ConvShape("jit_kl3_w9", 985, 2, 16, 9, 9, 80, 5, 5, 1, 2, 1),
+    # 1x1 with Kg >= 150: one-row tiles with the fewest k-blocks of KL = 4 / 6 / 8 (jit.cu choose())
+    datagen.ConvShape("jit_1x1_w17_kl6", 986, 2, 40, 17, 17, 192, 1, 1, 1, 0, 1),
+    datagen.ConvShape("jit_1x1_w10_kl8", 987, 2, 36, 10, 10, 256, 1, 1, 1, 0, 1),
+    datagen.ConvShape("jit_1x1_w12_kl6_ragged", 988, 2, 30, 12, 12, 300, 1, 1, 1, 0, 1),
+    datagen.ConvShape("jit_1x1_w20_kl4", 989, 2, 30, 20, 20, 256, 1, 1, 1, 0, 1),  # KL6/8 exceed 140 registers
 ]
+JIT_EXPECT = {"jit_1x1_w17_kl6": "_ty1_kl6_", "jit_1x1_w10_kl8": "_ty1_kl8_", "jit_1x1_w12_kl6_ragged": "_ty1_kl6_",
+              "jit_1x1_w20_kl4": "_kl4_"}
 
 
 @pytest.mark.parametrize("shp", JIT_SHAPES, ids=[s.name for s in JIT_SHAPES])
@@ -196,6 +203,7 @@ def test_jit_variant(sc, shp):
     conv = make_conv(sc, shp, w, b)
     vid, name = conv.variant
     assert vid == -1 and name.startswith("jit_"), name
+    assert JIT_EXPECT.get(shp.name, "") in name, name
     xd = torch.from_numpy(x).to(DEV)
     out = conv.forward(xd).cpu().numpy()
     ref, mass = oracle.conv_fp64(x, w, b, shp.stride, shp.pad, shp.groups)
@@ -215,3 +223,19 @@ def test_jit_variant(sc, shp):
             assert np.all(np.abs(o - ref) <= oracle.tolerance_sparse(mass))
         else:
             assert np.all(np.abs(o - ref) <= oracle.tolerance_dense_tf32(mass))
+
+
+def test_jit_force_rejects_invalid_parameters(sc, monkeypatch):
+    """SC_JIT_FORCE sets outside the kernel's limits fail plan creation (SC_ERR_UNSUPPORTED)
+    instead of running: 64 weight chunks of 16 channels (Cg = 1024), KL = 5 (no packing)."""
+    if not sc.lib().sc_jit_available():
+        pytest.skip("NVRTC not loadable")
+    shp = datagen.ConvShape("force_bad", 990, 1, 1024, 7, 7, 64, 1, 1, 1, 0, 1)
+    w, b = datagen.weights(shp)
+    for force, why in (("2,4,11,1,16,2,3,254", "63 weight chunks"), ("1,5,11,1,32,2,3,254", "KL must be")):
+        monkeypatch.setenv("SC_JIT_FORCE", force)
+        with pytest.raises(sc.SparseConvError) as e:
+            make_conv(sc, shp, w, b)
+        assert e.value.status == 3 and why in str(e.value), str(e.value)
+    monkeypatch.setenv("SC_JIT_FORCE", "2,4,11,1,17,2,3,254")  # 61 chunks: accepted
+    assert make_conv(sc, shp, w, b).variant[0] == -1

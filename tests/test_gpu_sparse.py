@@ -132,7 +132,7 @@ def test_integer_data_bitexact_table2(sc):
 
 
 # Stage-2 kernel a plan picks for the 1x1 Table 2 layers (tools/gen_gather.py VARIANTS: the
-# wide k-block tilings V53/V54/V55 need Kg >= KMIN, else the round-1 V43/V45).
+# wide k-block tilings V53-V56 for Kg >= 150, else the round-1 V43/V45).
 T2_1X1_VARIANT = {"GoogLeNet-Inception4a.1": 53, "GoogLeNet-Inception4a.2": 43, "GoogLeNet-Inception5a.1": 54,
                   "GoogLeNet-Inception5a.2": 55}
 
@@ -144,14 +144,20 @@ def test_table2_1x1_variant_choice(sc):
             assert make_conv(sc, shp, w, b).variant[0] == T2_1X1_VARIANT[shp.name], shp.name
 
 
-@pytest.mark.parametrize("k,wd,groups,want", [(151, 14, 1, 53), (149, 14, 1, 43), (201, 7, 1, 54), (199, 7, 1, 55),
-                                                (150, 7, 1, 55), (149, 7, 1, 45), (300, 7, 1, 54), (402, 7, 2, 54)])
+# (Kg, plane width, groups, variant): KL = the fewest k-blocks of 128 / 192 / 256 filters
+# (sc_internal.h wide_1x1_kl), Kg >= 150
+WIDE_CASES = [(151, 14, 1, 53), (149, 14, 1, 43), (256, 14, 1, 56), (300, 14, 1, 53), (400, 14, 1, 56),
+              (201, 7, 1, 54), (199, 7, 1, 54), (150, 7, 1, 55), (192, 7, 1, 55), (149, 7, 1, 45), (300, 7, 1, 55),
+              (201, 7, 2, 54)]
+
+
+@pytest.mark.parametrize("k,wd,groups,want", WIDE_CASES)
 def test_wide_kblock_1x1_ragged(sc, k, wd, groups, want):
-    """KL = 6 / 8 tiles (k-blocks of 192 / 256 channels) at the KMIN edges and with ragged
+    """KL = 6 / 8 tiles (k-blocks of 192 / 256 channels) at the rule's edges and with ragged
     last k-blocks (zero-padded weights, pack.cu) and groups: tolerance at s=0.9 on all
     outputs, stage-1 lists bit-exact, integer data bit-exact."""
-    shp = datagen.ConvShape(f"wide_kblock_{k}_{wd}_{groups}", 5000 + k + wd, 3, 38 * groups, wd, wd, k, 1, 1, 1, 0,
-                            groups)
+    shp = datagen.ConvShape(f"wide_kblock_{k}_{wd}_{groups}", 5000 + k + wd, 3, 38 * groups, wd, wd, k * groups, 1, 1,
+                            1, 0, groups)
     x = datagen.activations(shp, 0.9, seed=k)
     w, b = datagen.weights(shp, seed=k)
     conv = make_conv(sc, shp, w, b, max_batch=4)

@@ -59,10 +59,12 @@ VARIANTS = [
     (47, "r5s5p2_w7_ty2_kl2_sl2p126", 5, 5, 2, 7, 2, 2, 11, 1, 16, 2, None, 2, 126),       # Inception5b.5
     # round 2: 1x1 layers with one dispatch per nonzero for all of a k-block of 32*KL >= Kg
     # channels (KL = 6, 8; no halo, so the tile height buys no reuse: TY = 1), 32-channel
-    # weight chunks (profiles/r2_t2_kl68_tune.txt), replacing V48 / V49
+    # weight chunks (profiles/r2_t2_kl68_tune.txt), replacing V48 / V49.  KMIN > 0 marks them:
+    # they match only where KL is sc_internal.h wide_1x1_kl's choice (fewest k-blocks)
     (53, "r1s1p0_w14_ty1_kl6_ch32sl2_k150", 1, 1, 0, 14, 1, 6, 11, 1, 32, 2, None, 2, 254, 1, 150),  # Inception4a.1
-    (54, "r1s1p0_w7_ty1_kl8_ch32s3_k200", 1, 1, 0, 7, 1, 8, 11, 1, 32, 3, None, 3, 254, 1, 200),     # Inception5a.1
+    (54, "r1s1p0_w7_ty1_kl8_ch32s3_k150", 1, 1, 0, 7, 1, 8, 11, 1, 32, 3, None, 3, 254, 1, 150),     # Inception5a.1
     (55, "r1s1p0_w7_ty1_kl6_ch32s3sl2p510_k150", 1, 1, 0, 7, 1, 6, 11, 1, 32, 3, None, 2, 510, 1, 150),  # Inception5a.2
+    (56, "r1s1p0_w14_ty1_kl8_ch32sl2_k150", 1, 1, 0, 14, 1, 8, 11, 1, 32, 2, None, 2, 254, 1, 150),  # 14x14, Kg 193-256
 ]
 
 # Superseded round-1 tilings (slower than the shipped variant of the same shape, DESIGN.md
@@ -93,7 +95,7 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 51, 52, 33, 50, 53, 54, 55]  # 53/54/55 need Kg >= KMIN (54 before 55)
+PRIORITY = [21, 51, 52, 33, 50, 53, 54, 55, 56]  # 53-56: Kg >= KMIN and KL = wide_1x1_kl
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):
