@@ -370,6 +370,56 @@ def timed_steps(torch, stream, graphs, steps, warmup, ws, dev):
     return shard.max_over_ranks(e0.elapsed_time(e1), ws, dev) / steps
 
 
+PIPE_ROUND = 12  # batches per sparse_conv_forward_batches graph (at least; whole rounds of the sets)
+
+
+def batch_graphs(torch, stream, conv, xs, outs, counts):
+    """CUDA graphs of sparse_conv_forward_batches over c batches cycling through the sets,
+    one per c in counts."""
+    conv.reserve_batches()
+    gs = {}
+    with torch.cuda.stream(stream):
+        for c in sorted(set(counts)):
+            bx = [xs[i % len(xs)] for i in range(c)]
+            bo = [outs[i % len(outs)] for i in range(c)]
+            conv.forward_batches(bx, bo, stream=stream)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                conv.forward_batches(bx, bo, stream=stream)
+            gs[c] = g
+    return gs
+
+
+def pipe_round(nsets):
+    return nsets * -(-PIPE_ROUND // nsets)
+
+
+def timed_batches(torch, stream, gs, nsets, steps, warmup, ws, dev):
+    """Like timed_steps, for pipelined steps: W untimed + K timed batches as replays of
+    sparse_conv_forward_batches graphs of pipe_round(nsets) batches (a last shorter one for
+    the remainder); each replay drains the pipeline at its end."""
+    rnd = pipe_round(nsets)
+
+    def seq(k):
+        return [gs[rnd]] * (k // rnd) + ([gs[k % rnd]] if k % rnd else [])
+
+    with torch.cuda.stream(stream):
+        for g in seq(warmup):
+            g.replay()
+        stream.synchronize()
+        shard.barrier(ws)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for g in seq(steps):
+            g.replay()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize(dev)
+    return shard.max_over_ranks(e0.elapsed_time(e1), ws, dev) / steps
+
+
 def run_single(args, torch, dev, ws, rank, sc):
     shp = datagen.CONFIGS[args.config]
     n = shp.n
@@ -402,8 +452,17 @@ def run_single(args, torch, dev, ws, rank, sc):
                 with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
                     conv.forward(xs[si], outs[si], stream=stream)
                 graphs.append(g)
-        res = {"ms_per_step": timed_steps(torch, stream, graphs, steps, warmup, ws, dev)}
+        res = {"unpipelined_ms_per_step": timed_steps(torch, stream, graphs, steps, warmup, ws, dev)}
         del graphs
+        if args.no_pipeline:
+            res["ms_per_step"] = res["unpipelined_ms_per_step"]
+        else:
+            # the step as a user with a stream of batches runs it: sparse_conv_forward_batches
+            # overlaps batch b+1's stage 1 (and first stage-2 wave) with batch b's last stage-2 wave
+            rnd = pipe_round(nsets)
+            gs = batch_graphs(torch, stream, conv, xs, outs, [rnd, steps % rnd or rnd, warmup % rnd or rnd])
+            res["ms_per_step"] = timed_batches(torch, stream, gs, nsets, steps, warmup, ws, dev)
+            del gs
         # per-stage and dense-path times on the same rotating sets as the step (cold L2, like the
         # step itself); the set-0 graph replays (L2-warm) are reported beside them, labelled
         rot = max(steps, 2 * nsets)
@@ -512,8 +571,16 @@ def run_ours(args):
         "config": {"workload": workload_name(shp, s_head, n), "global_batch": n * ws, "parallelism": f"dp{ws}",
                    **shared_gpu_note(ws),
                    "l2": f"{v['nsets']} rotating input/output sets ({v['set_mib']:.0f} MiB > 2x L2)",
-                   "timing": "CUDA events around K CUDA-graph replays (one sparse_conv_forward each), max over ranks",
+                   "timing": ("CUDA events around K CUDA-graph replays (one sparse_conv_forward each), max over ranks"
+                              if args.no_pipeline else
+                              "CUDA events around K batches run as CUDA-graph replays of sparse_conv_forward_batches "
+                              f"of {pipe_round(v['nsets'])} batches cycling the {v['nsets']} rotating sets "
+                              "(batch b+1's stage 1 overlaps batch b's "
+                              "stage 2; every batch's output identical to sparse_conv_forward), max over ranks"),
                    "realized_sparsity": round(v["realized_s"], 5), "variant": vname},
+        "pipelined": not args.no_pipeline,
+        "unpipelined_ms_per_step": round(v["unpipelined_ms_per_step"], 5),
+        "unpipelined_value": round(gflops(v["dense"], v["unpipelined_ms_per_step"]), 2),
         "nonzero_mac_per_s": round(v["exact"] * ws / (v["ms_per_step"] * 1e-3), 1),
         "pct_roofline": round(100 * t_roof / (v["ms_per_step"] * 1e-3), 2),
         "roofline_step": {"t_roof_us": round(t_roof * 1e6, 3), "t_fp32_us": round(t_fp32 * 1e6, 3),
@@ -544,6 +611,7 @@ def run_ours(args):
         "sweep": {str(s): {"value": round(gflops(r["dense"], r["ms_per_step"]), 2),
                            "nonzero_mac_per_s": round(r["exact"] * ws / (r["ms_per_step"] * 1e-3), 1),
                            "ms_per_step": round(r["ms_per_step"], 5),
+                           "unpipelined_ms_per_step": round(r["unpipelined_ms_per_step"], 5),
                            "pct_roofline": round(100 * summary(r)[3] / (r["ms_per_step"] * 1e-3), 2),
                            "gather_frac_fp32": round(2 * r["exact"] / (r["gather_us"] * 1e-6) / 1e12
                                                      / FP32_PEAK_TFLOPS, 4),
@@ -962,6 +1030,8 @@ def main():
     ap.add_argument("--sparsity", default=None,
                     help="input sparsity (default per config: C1 0.9, C3 'channel', else 0.95)")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="time each step as one sparse_conv_forward (no overlap across batches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--table2", action="store_true", help="paper Table 2 layers: sparse vs dense on B200")
     ap.add_argument("--table2-batch", type=int, default=128)

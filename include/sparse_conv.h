@@ -121,6 +121,30 @@ sc_status sparse_conv_create(const sc_conv_params *params, const float *d_weight
 sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *d_out,
                               sc_stream_t stream);
 
+/* A sequence of nbatch independent batches of n images each: d_in[b] / d_out[b]
+ * (host arrays of nbatch device pointers, each buffer as in sparse_conv_forward)
+ * hold batch b.  Each batch's outputs are bit-identical to sparse_conv_forward on
+ * that batch, since the same kernels run.  The calls are pipelined across batches:
+ * - Batch b+1's stage 1 runs on a low-priority plan-owned stream while batch b's
+ *   stage 2 is still running, so it fills the SMs that stage 2's last wave leaves idle.
+ * - The plan keeps two stage-1 workspaces and alternates between them.
+ * - Stage-2 launches alternate between two high-priority plan-owned streams, so
+ *   batch b+1's stage 2 can start in batch b's last wave.
+ * The work starts after everything already queued on `stream`, and `stream`
+ * resumes after the last batch.  No host synchronization, so it can be captured in
+ * a CUDA graph.  The first call creates the second workspace and the streams, so it
+ * must not be made while `stream` is capturing (SC_ERR_INVALID_ARGUMENT);
+ * sparse_conv_reserve_batches does that ahead of time.  nbatch == 1 is exactly
+ * sparse_conv_forward.  The same plan must not run another forward concurrently.
+ * Why: a stage-2 CTA holds a whole SM
+ * (registers and shared memory), and C2 needs 1.66 waves of them. */
+sc_status sparse_conv_forward_batches(sc_plan plan, int32_t nbatch, int64_t n, const float *const *d_in,
+                                      float *const *d_out, sc_stream_t stream);
+
+/* Allocate what sparse_conv_forward_batches needs (second stage-1 workspace,
+ * streams, events); idempotent. */
+sc_status sparse_conv_reserve_batches(sc_plan plan);
+
 /* Dense comparison path: implicit GEMM on tcgen05 tensor cores,
  * operands rounded to TF32 (cvt.rna), fp32 accumulation.  Two launches: the
  * input is transposed to a plan-owned channels-last TF32 copy, then every

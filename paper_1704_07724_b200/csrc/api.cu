@@ -55,6 +55,15 @@ struct sc_plan_s {
     static constexpr int kHostComp = 4;  // compute streams (chunks use disjoint workspace slices)
     cudaStream_t hs[2 + kHostComp] = {};  // [0] copy-in, [1] copy-out, [2..] compute
     cudaEvent_t ev_in[kHostChunks] = {}, ev_comp[kHostChunks] = {}, ev_start = nullptr, ev_done = nullptr;
+    // sparse_conv_forward_batches (sparse_conv_reserve_batches): a second stage-1 workspace, a
+    // low-priority stage-1 stream [0] and two high-priority stage-2 streams [1], [2]
+    uint2* entries2 = nullptr;
+    uint32_t* offs2 = nullptr;
+    uint32_t* cnt2 = nullptr;
+    uint2* plist2 = nullptr;
+    uint32_t* prow2 = nullptr;
+    cudaStream_t bs[3] = {};
+    cudaEvent_t bev_fork = nullptr, bev_s1 = nullptr, bev_g[2] = {};
 };
 
 namespace {
@@ -223,6 +232,15 @@ void free_plan(sc_plan_s* p) {
     if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->bws);
     cudaFree(p->bdt);
+    cudaFree(p->entries2);
+    cudaFree(p->offs2);
+    cudaFree(p->cnt2);
+    cudaFree(p->plist2);
+    cudaFree(p->prow2);
+    for (auto& h : p->bs)
+        if (h) cudaStreamDestroy(h);
+    for (cudaEvent_t ev : {p->bev_fork, p->bev_s1, p->bev_g[0], p->bev_g[1]})
+        if (ev) cudaEventDestroy(ev);
     delete p;
 }
 
@@ -281,6 +299,39 @@ cudaError_t ensure_host_pipeline(sc_plan_s* p) {
         if ((e = mk(&p->ev_in[i])) != cudaSuccess || (e = mk(&p->ev_comp[i])) != cudaSuccess) return e;
     if ((e = mk(&p->ev_start)) != cudaSuccess) return e;
     return mk(&p->ev_done);
+}
+
+bool batches_ready(const sc_plan_s* p) {
+    return p->bs[0] && p->bs[1] && p->bs[2] && p->bev_fork && p->bev_s1 && p->bev_g[0] && p->bev_g[1] &&
+           p->entries2 && p->offs2 && (!sc::compact_uses_counts(p->g) || (p->cnt2 && p->plist2 && p->prow2));
+}
+
+cudaError_t ensure_batches(sc_plan_s* p) {
+    const Geometry& g = p->g;
+    cudaError_t e = cudaSuccess;
+    const size_t ebytes = sizeof(uint2) * (g.N * g.tiles * g.cap + 2);
+    if (!p->entries2) {
+        if ((e = cudaMalloc(&p->entries2, ebytes)) != cudaSuccess) return e;
+        // as for the plan's own streams: slack is never interpreted, but keep it initialised
+        if ((e = cudaMemset(p->entries2, 0, ebytes)) != cudaSuccess) return e;
+    }
+    if (!p->offs2 && (e = cudaMalloc(&p->offs2, sizeof(uint32_t) * g.N * g.tiles * (g.C + 1))) != cudaSuccess)
+        return e;
+    if (sc::compact_uses_counts(g)) {
+        if (!p->cnt2 && (e = cudaMalloc(&p->cnt2, sizeof(uint32_t) * g.N * g.tiles * g.C)) != cudaSuccess) return e;
+        if (!p->plist2 && (e = cudaMalloc(&p->plist2, sizeof(uint2) * g.N * g.C * g.H * g.W)) != cudaSuccess) return e;
+        if (!p->prow2 && (e = cudaMalloc(&p->prow2, sizeof(uint32_t) * g.N * g.C * (g.H + 1))) != cudaSuccess)
+            return e;
+    }
+    int least = 0, greatest = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&least, &greatest)) != cudaSuccess) return e;
+    for (int i = 0; i < 3; ++i)
+        if (!p->bs[i] &&
+            (e = cudaStreamCreateWithPriority(&p->bs[i], cudaStreamNonBlocking, i == 0 ? least : greatest)) != cudaSuccess)
+            return e;
+    for (cudaEvent_t* ev : {&p->bev_fork, &p->bev_s1, &p->bev_g[0], &p->bev_g[1]})
+        if (!*ev && (e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    return cudaDeviceSynchronize();  // the workspace memset
 }
 
 // Best-of-3 device time (us) of one path on the staged input (one untimed run first).
@@ -476,6 +527,65 @@ sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float* d_in, float*
     sc_status st = sparse_conv_compact(plan, n, d_in, stream);
     if (st != SC_OK) return st;
     return sparse_conv_gather(plan, n, d_out, stream);
+}
+
+sc_status sparse_conv_reserve_batches(sc_plan plan) {
+    if (!plan) return fail(SC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    DeviceGuard guard(plan->device);
+    const cudaError_t e = ensure_batches(plan);
+    return e == cudaSuccess ? SC_OK : cuda_fail(e, "sparse_conv_reserve_batches");
+}
+
+sc_status sparse_conv_forward_batches(sc_plan plan, int32_t nbatch, int64_t n, const float* const* d_in,
+                                      float* const* d_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if (nbatch < 1 || !d_in || !d_out)
+        return fail(SC_ERR_INVALID_ARGUMENT, "nbatch=%d: need nbatch >= 1 and the d_in / d_out arrays", (int)nbatch);
+    for (int32_t b = 0; b < nbatch; ++b)
+        if ((st = check_dev_ptr(plan, d_in[b], "d_in[b]")) != SC_OK || (st = check_dev_ptr(plan, d_out[b], "d_out[b]")) != SC_OK)
+            return st;
+    if (nbatch == 1) return sparse_conv_forward(plan, n, d_in[0], d_out[0], stream);
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if (!batches_ready(plan)) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(SC_ERR_INVALID_ARGUMENT,
+                        "first sparse_conv_forward_batches under stream capture: call sparse_conv_reserve_batches first");
+        if ((e = ensure_batches(plan)) != cudaSuccess) return cuda_fail(e, "sparse_conv_forward_batches setup");
+    }
+    const Geometry& g = plan->g;
+    // fork: every plan stream starts after the work already queued on `stream`
+    if ((e = cudaEventRecord(plan->bev_fork, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    for (cudaStream_t b : plan->bs)
+        if ((e = cudaStreamWaitEvent(b, plan->bev_fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    cudaStream_t s1 = plan->bs[0];
+    for (int32_t b = 0; b < nbatch; ++b) {
+        const int slot = b & 1;
+        uint2* entries = slot ? plan->entries2 : plan->entries;
+        uint32_t* offs = slot ? plan->offs2 : plan->offs;
+        uint32_t* cnt = slot ? plan->cnt2 : plan->cnt;
+        uint2* plist = slot ? plan->plist2 : plan->plist;
+        uint32_t* prow = slot ? plan->prow2 : plan->prow;
+        cudaStream_t s2 = plan->bs[1 + slot];
+        // stage 1 of batch b overwrites the workspace batch b-2's stage 2 read
+        if (b >= 2 && (e = cudaStreamWaitEvent(s1, plan->bev_g[slot], 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+        if ((e = sc::launch_compact(g, n, d_in[b], cnt, plist, prow, entries, offs, s1)) != cudaSuccess)
+            return cuda_fail(e, "compact launch");
+        if ((e = cudaEventRecord(plan->bev_s1, s1)) != cudaSuccess || (e = cudaStreamWaitEvent(s2, plan->bev_s1, 0)) != cudaSuccess)
+            return cuda_fail(e, "stage-1 event");
+        if ((e = launch_stage2(plan, n, entries, offs, d_out[b], nullptr, nullptr, s2)) != cudaSuccess)
+            return cuda_fail(e, "gather launch");
+        if ((e = cudaEventRecord(plan->bev_g[slot], s2)) != cudaSuccess) return cuda_fail(e, "event record");
+    }
+    // join: the last stage 2 of each stream (every stage 1 precedes a stage 2 of its batch)
+    for (int slot = 0; slot < 2; ++slot)
+        if ((e = cudaStreamWaitEvent(s, plan->bev_g[slot], 0)) != cudaSuccess) return cuda_fail(e, "stream join");
+    plan->lists_layout = 0;  // the list views describe sparse_conv_forward / sparse_conv_compact only
+    return SC_OK;
 }
 
 sc_status dense_conv_forward(sc_plan plan, int64_t n, const float* d_in, float* d_out, sc_stream_t stream) {

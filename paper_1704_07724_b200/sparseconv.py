@@ -25,7 +25,7 @@ EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forwar
            "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
            "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
            "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward", "sc_jit_variant_source",
-           "sc_jit_available", "sparse_conv_plane_lists")
+           "sc_jit_available", "sparse_conv_plane_lists", "sparse_conv_forward_batches", "sparse_conv_reserve_batches")
 SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
@@ -70,6 +70,8 @@ def lib():
         L.sparse_conv_compact.argtypes = [vp, i64, vp, vp]
         L.sparse_conv_forward_chain.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64, vp, ctypes.POINTER(vp), vp]
         L.sparse_conv_gather.argtypes = [vp, i64, vp, vp]
+        L.sparse_conv_forward_batches.argtypes = [vp, ctypes.c_int32, i64, ctypes.POINTER(vp), ctypes.POINTER(vp), vp]
+        L.sparse_conv_reserve_batches.argtypes = [vp]
         L.sparse_conv_destroy.argtypes = [vp]
         L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
         L.sparse_conv_kernel_variant.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_char_p)]
@@ -164,6 +166,25 @@ class SparseConv:
         return out
 
     __call__ = forward
+
+    def forward_batches(self, xs, outs=None, stream=None):
+        """sparse_conv_forward_batches: independent batches xs[b] -> outs[b] (same batch size),
+        batch b+1's stage 1 overlapping batch b's stage 2."""
+        n = xs[0].shape[0]
+        if outs is None:
+            outs = [torch.empty((n,) + self.out_shape, device=self.device, dtype=torch.float32) for _ in xs]
+        if len(outs) != len(xs):
+            raise ValueError("xs and outs differ in length")
+        for x, o in zip(xs, outs):
+            _check_tensor(x, "x", self.device, (n,) + self.in_shape)
+            _check_tensor(o, "out", self.device, (n,) + self.out_shape)
+        ins = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        ous = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        _check(lib().sparse_conv_forward_batches(self._plan, len(xs), n, ins, ous, _stream_handle(stream)))
+        return outs
+
+    def reserve_batches(self):
+        _check(lib().sparse_conv_reserve_batches(self._plan))
 
     def dense_forward(self, x, out=None, stream=None):
         n = x.shape[0]
