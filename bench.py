@@ -791,9 +791,35 @@ def run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
             with torch.cuda.graph(g, stream=main, capture_error_mode="relaxed"):
                 step(si)
             graphs.append(g)
+    gs = {}
+    if not args.no_pipeline:
+        # pipelined steps: each layer's batches through sparse_conv_forward_batches on its stream
+        def rounds(c):
+            ev = torch.cuda.Event()
+            ev.record(main)
+            for j in range(2):
+                side[j].wait_event(ev)
+                convs[j].forward_batches([xs[i % nsets][j] for i in range(c)], [outs[i % nsets][j] for i in range(c)],
+                                         stream=side[j])
+                done = torch.cuda.Event()
+                done.record(side[j])
+                main.wait_event(done)
+
+        for c in convs:
+            c.reserve_batches()
+        rnd = pipe_round(nsets)
+        with torch.cuda.stream(main):
+            for c in sorted({rnd, args.steps % rnd or rnd, args.warmup % rnd or rnd}):
+                rounds(c)
+                main.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=main, capture_error_mode="relaxed"):
+                    rounds(c)
+                gs[c] = g
     clocks = ClockSampler(dev.index)
     with clocks:
-        ms = timed_steps(torch, main, graphs, args.steps, args.warmup, ws, dev)
+        ms_unpiped = timed_steps(torch, main, graphs, args.steps, args.warmup, ws, dev)
+        ms = ms_unpiped if args.no_pipeline else timed_batches(torch, main, gs, nsets, args.steps, args.warmup, ws, dev)
         alone = [rotating_time_us(torch, main, [lambda i=i, j=j: convs[j].forward(xs[i][j], outs[i][j], stream=main)
                                                for i in range(nsets)], max(args.steps, 2 * nsets))
                  for j in range(2)]
@@ -801,7 +827,7 @@ def run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
                                                                                              stream=main)
                                                      for i in range(nsets)], max(args.steps, 2 * nsets))
                        for j in range(2)]
-    del graphs
+    del graphs, gs
     dense = sum(c[0] for cs in counts for c in cs) / nsets
     exact = sum(c[1] for cs in counts for c in cs) / nsets
     nbytes = sum(algorithmic_bytes(shp, n, sum(cs[j][2] for cs in counts) / nsets,
@@ -816,8 +842,14 @@ def run_pair(args, torch, dev, ws, rank, sc, hbm_gbs, peak_kind):
                                f"{workload_name(shps[1], s, n)}",
                    "global_batch": n * ws, "parallelism": f"dp{ws}", **shared_gpu_note(ws),
                    "l2": f"{nsets} rotating input/output sets ({nsets * per_set / 2 ** 20:.0f} MiB > 2x L2)",
-                   "timing": "CUDA events around K graph replays (both layers forked onto two streams), max over ranks",
+                   "timing": ("CUDA events around K graph replays (both layers forked onto two streams), max over ranks"
+                              if args.no_pipeline else
+                              f"CUDA events around K batches as CUDA-graph replays of {pipe_round(nsets)} batches: both "
+                              "layers forked onto two streams, each through sparse_conv_forward_batches (batch b+1's "
+                              "stage 1 overlaps batch b's stage 2), max over ranks"),
                    "variants": [c.variant[1] for c in convs]},
+        "pipelined": not args.no_pipeline,
+        "unpipelined_ms_per_step": round(ms_unpiped, 5),
         "nonzero_mac_per_s": round(exact * ws / (ms * 1e-3), 1),
         "pct_roofline": round(100 * t_roof / (ms * 1e-3), 2),
         "roofline_step": {"t_roof_us": round(t_roof * 1e6, 3), "t_fp32_us": round(t_fp32 * 1e6, 3),
