@@ -179,7 +179,14 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, f
  * turns into the same R9 streams without re-reading a dense tensor.  Returns
  * SC_ERR_UNSUPPORTED if such an intermediate layer cannot emit lists (its
  * stage-2 kernel is the generic one or a KL=1 variant) and d_outs[l] is NULL.
- * Stream-ordered, asynchronous, graph-capturable like sparse_conv_forward. */
+ * Stream-ordered, asynchronous, graph-capturable like sparse_conv_forward.
+ * For n >= 256 the chain runs as 2 chunks of whole images (multiples of 4),
+ * each through all layers in its own image slice of every plan's workspace. The
+ * chunks use two streams owned by plans[0], so one chunk's last, partly filled
+ * stage-2 wave of a layer overlaps the other chunk's work. The
+ * SC_CHAIN_CHUNKS env var (measurement knob, 1-8) changes the count. The first
+ * chunked call creates those streams, so it must not be made while `stream` is
+ * capturing (SC_ERR_INVALID_ARGUMENT). */
 sc_status sparse_conv_forward_chain(const sc_plan *plans, int32_t nplans, int64_t n, const float *d_in,
                                     float *const *d_outs, sc_stream_t stream);
 

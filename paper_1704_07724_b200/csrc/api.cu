@@ -384,6 +384,51 @@ sc_status check_forward(sc_plan plan, int64_t n) {
     return SC_OK;
 }
 
+// Layers of a chain for images [img0, img0 + n) on stream s: each plan's workspace slice of
+// those images (image-major), layer l+1's lists emitted by layer l's gather when it can.
+sc_status enqueue_chain(const sc_plan* plans, int32_t nplans, int64_t n, int64_t img0, const float* d_in,
+                        float* const* d_outs, cudaStream_t s) {
+    bool lists_ready = false;  // plans[l]'s row lists were written by layer l-1's gather
+    for (int l = 0; l < nplans; ++l) {
+        sc_plan_s* p = plans[l];
+        const Geometry& g = p->g;
+        cudaError_t e;
+        uint32_t* cnt = p->cnt ? p->cnt + img0 * g.tiles * g.C : nullptr;
+        uint2* entries = p->entries + img0 * g.tiles * g.cap;
+        uint32_t* offs = p->offs + img0 * g.tiles * (g.C + 1);
+        uint2* plist = p->plist ? p->plist + img0 * g.C * g.H * g.W : nullptr;
+        const float* in_prev = l > 0 && d_outs[l - 1] ? d_outs[l - 1] + img0 * g.C * g.H * g.W : nullptr;
+        if (l == 0) {
+            uint32_t* prow = p->prow ? p->prow + img0 * g.C * (g.H + 1) : nullptr;
+            e = sc::launch_compact(g, n, d_in + img0 * g.C * g.H * g.W, cnt, plist, prow, entries, offs, s);
+        } else if (lists_ready) {
+            // the producer's per-(plane, row) slots and row counts (rcnt: C*H per image)
+            uint32_t* rcnt = p->prow + img0 * g.C * g.H;
+            e = sc::launch_compact_from_rows(g, n, cnt, plist, rcnt, entries, offs, s);
+        } else {
+            if (!in_prev)
+                return fail(SC_ERR_UNSUPPORTED, "layer %d cannot emit chained lists: d_outs[%d] is required", l - 1,
+                            l - 1);
+            uint32_t* prow = p->prow ? p->prow + img0 * g.C * (g.H + 1) : nullptr;
+            e = sc::launch_compact(g, n, in_prev, cnt, plist, prow, entries, offs, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "chain stage 1");
+        if (!lists_ready) p->lists_layout = (sc::compact_uses_counts(g) && p->plist && p->prow) ? 1 : 0;
+        sc_plan_s* next = l + 1 < nplans ? plans[l + 1] : nullptr;
+        const bool emit = next && p->variant > 0 && sc::gather_fast_can_emit(p->variant) &&
+                          sc::compact_uses_counts(next->g) && next->plist && next->prow;
+        float* out = d_outs[l] ? d_outs[l] + img0 * g.K * g.Ho * g.Wo : nullptr;
+        if (!emit && !out) return fail(SC_ERR_UNSUPPORTED, "layer %d needs an output buffer (no list emission)", l);
+        uint2* rows_next = emit ? next->plist + img0 * next->g.C * next->g.H * next->g.W : nullptr;
+        uint32_t* rcnt_next = emit ? next->prow + img0 * next->g.C * next->g.H : nullptr;
+        e = launch_stage2(p, n, entries, offs, out, rows_next, rcnt_next, s);
+        if (e != cudaSuccess) return cuda_fail(e, "chain gather");
+        if (emit) next->lists_layout = 2;
+        lists_ready = emit;
+    }
+    return SC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -696,33 +741,39 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
         if (d_outs[l] && (st = check_dev_ptr(plans[0], d_outs[l], "d_outs[l]")) != SC_OK) return st;
     DeviceGuard guard(plans[0]->device);
     cudaStream_t s = (cudaStream_t)stream;
-    bool lists_ready = false;  // plans[l]'s row lists were written by layer l-1's gather
-    for (int l = 0; l < nplans; ++l) {
-        sc_plan_s* p = plans[l];
-        cudaError_t e;
-        if (l == 0) {
-            e = sc::launch_compact(p->g, n, d_in, p->cnt, p->plist, p->prow, p->entries, p->offs, s);
-        } else if (lists_ready) {
-            e = sc::launch_compact_from_rows(p->g, n, p->cnt, p->plist, p->prow, p->entries, p->offs, s);
-        } else {
-            if (!d_outs[l - 1])
-                return fail(SC_ERR_UNSUPPORTED, "layer %d cannot emit chained lists: d_outs[%d] is required", l - 1,
-                            l - 1);
-            e = sc::launch_compact(p->g, n, d_outs[l - 1], p->cnt, p->plist, p->prow, p->entries, p->offs, s);
-        }
-        if (e != cudaSuccess) return cuda_fail(e, "chain stage 1");
-        if (!lists_ready) p->lists_layout = (sc::compact_uses_counts(p->g) && p->plist && p->prow) ? 1 : 0;
-        sc_plan_s* next = l + 1 < nplans ? plans[l + 1] : nullptr;
-        const bool emit = next && p->variant > 0 && sc::gather_fast_can_emit(p->variant) &&
-                          sc::compact_uses_counts(next->g) && next->plist && next->prow;
-        float* out = d_outs[l];
-        if (!emit && !out) return fail(SC_ERR_UNSUPPORTED, "layer %d needs an output buffer (no list emission)", l);
-        e = launch_stage2(p, n, p->entries, p->offs, out, emit ? next->plist : nullptr, emit ? next->prow : nullptr,
-                          s);
-        if (e != cudaSuccess) return cuda_fail(e, "chain gather");
-        if (emit) next->lists_layout = 2;
-        lists_ready = emit;
+    // Large batches run as chunks of whole images on two plan-owned streams (every workspace is
+    // image-major): one chunk's layer tails (the last, partly filled wave of each gather) overlap
+    // another chunk's layers.  SC_CHAIN_CHUNKS (measurement knob): chunks, 1 = none.
+    static const int max_chunks = [] {
+        const char* v = getenv("SC_CHAIN_CHUNKS");
+        const int c = v ? atoi(v) : 2;  // C5 (N=1024): 1 / 2 / 4 / 8 chunks 4.03 / 3.96 / 3.99 / 4.31 ms
+        return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
+    }();
+    int chunks = (int)(n / 128 < max_chunks ? n / 128 : max_chunks);  // chunks of >= 128 images
+    if (chunks < 2) return enqueue_chain(plans, nplans, n, 0, d_in, d_outs, s);
+    sc_plan_s* p0 = plans[0];
+    cudaError_t e;
+    if (!p0->hs[2] || !p0->hs[3] || !p0->ev_start || !p0->ev_comp[chunks - 1]) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(SC_ERR_INVALID_ARGUMENT, "first chunked sparse_conv_forward_chain under stream capture: run it "
+                                                 "once outside capture (creates the plan's streams)");
+        if ((e = ensure_host_pipeline(p0)) != cudaSuccess) return cuda_fail(e, "chain streams");
     }
+    if ((e = cudaEventRecord(p0->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    for (int k = 2; k < 4; ++k)
+        if ((e = cudaStreamWaitEvent(p0->hs[k], p0->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t c0 = (n * c / chunks) & ~(int64_t)3, c1 = c + 1 == chunks ? n : ((n * (c + 1) / chunks) & ~(int64_t)3);
+        cudaStream_t cs = p0->hs[2 + (c & 1)];
+        sc_status st2 = enqueue_chain(plans, nplans, c1 - c0, c0, d_in, d_outs, cs);
+        if (st2 != SC_OK) return st2;
+        if ((e = cudaEventRecord(p0->ev_comp[c], cs)) != cudaSuccess) return cuda_fail(e, "event record");
+    }
+    // join: the last chunk of each stream (stream order covers the earlier ones)
+    for (int c = chunks - 2; c < chunks; ++c)
+        if ((e = cudaStreamWaitEvent(s, p0->ev_comp[c], 0)) != cudaSuccess) return cuda_fail(e, "stream join");
     return SC_OK;
 }
 

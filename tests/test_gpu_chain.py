@@ -69,7 +69,7 @@ def _chain_setup(n):
     return sc, layers, weights, convs, x
 
 
-@pytest.mark.parametrize("n", [3, 64])
+@pytest.mark.parametrize("n", [3, 64, 260, 512])  # n >= 256: chunks of images on two streams
 def test_chain_fused_lists_match_compaction_and_oracle(n):
     """f1: intermediate layers emit the next layer's stage-1 lists from
     their epilogue.  With the intermediate outputs also materialised, every
