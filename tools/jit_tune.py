@@ -52,11 +52,19 @@ if os.environ.get("TUNE_GRID"):  # "2:4,1:4" = (TY, KL) pairs
 nws, chs, stages = env_list("TUNE_NWS", nws), env_list("TUNE_CHS", chs), env_list("TUNE_STAGES", stages)
 slots, pieces = env_list("TUNE_SLOTS", slots), env_list("TUNE_PIECES", pieces)
 full = cfg.startswith("T2:") or bool(os.environ.get("TUNE_FULL"))  # time the whole forward (the tile height changes stage 1 too)
+pipe = bool(os.environ.get("TUNE_PIPE"))  # time per batch of 12 batches through forward_batches (pipelined steps)
+out2 = torch.empty_like(out)
+
+
+def pipe_time(conv):
+    xs, outs = [x] * 12, [out, out2] * 6  # batches b, b+2 share a stage-2 stream, so an output buffer
+    conv.reserve_batches()
+    return dev_time_us(lambda: conv.forward_batches(xs, outs), reps=5) / 12
 os.environ.pop("SC_JIT_FORCE", None)
 base = sc.SparseConv(torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), shp.n, shp.c, shp.h, shp.w,
                      shp.stride, shp.pad, shp.groups)
-tb = dev_time_us(lambda: base.forward(x, out), reps=10) if full else None
-print("shipped", base.variant, f"forward {tb:.1f} us" if tb else "", flush=True)
+tb = pipe_time(base) if pipe else (dev_time_us(lambda: base.forward(x, out), reps=10) if full else None)
+print("shipped", base.variant, f"{'pipelined' if pipe else 'forward'} {tb:.1f} us" if tb else "", flush=True)
 del base
 res = []
 for (ty, kl), nw, ch, st, sl, pc in itertools.product(grid, nws, chs, stages, slots, pieces):
@@ -73,7 +81,9 @@ for (ty, kl), nw, ch, st, sl, pc in itertools.product(grid, nws, chs, stages, sl
     torch.cuda.synchronize()
     o = out.cpu().numpy()
     worst = max(float((np.abs(o[i:i + 1] - r) / oracle.tolerance_sparse(m)).max()) for i, (r, m) in refs.items())
-    if full:
+    if pipe:
+        t = pipe_time(conv)
+    elif full:
         t = dev_time_us(lambda: conv.forward(x, out), reps=10)
     else:
         conv.compact(x)

@@ -95,5 +95,16 @@ cap = torch.cuda.Stream()
 with torch.cuda.graph(g, stream=cap):
     library(graph_k, cap)
 print(f"forward_batches graph of {graph_k} {timed(lambda k: [g.replay() for _ in range(k // graph_k)], graph_k * 2):8.1f} us/batch")
+def gather_only(k):  # stage 2 alone, back to back on the two high-priority streams (stage 1 done once)
+    for g in G:
+        g.wait_stream(cur)
+    for i in range(k):
+        plans[0].gather(shp.n, outs[i % nsets], stream=G[i % 2])
+    for g in G:
+        cur.wait_stream(g)
+
+
+plans[0].compact(xs[0], stream=cur)
+print(f"stage 2 only, 2 G    {timed(gather_only, K):8.1f} us/batch")
 print(f"pipelined 1 G stream {timed(lambda k: pipelined(k, 1), K):8.1f} us/batch")
 print(f"pipelined no prio    {timed(lambda k: pipelined(k, 2, False), K):8.1f} us/batch")
