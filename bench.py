@@ -420,6 +420,24 @@ def timed_batches(torch, stream, gs, nsets, steps, warmup, ws, dev):
     return shard.max_over_ranks(e0.elapsed_time(e1), ws, dev) / steps
 
 
+def dense_two_stream_us(torch, stream, convs, xs, outs):
+    """Dense path per batch with the same cross-batch overlap the sparse steps get: two plans
+    (each its own channels-last workspace), batches alternating between two streams, one
+    CUDA graph over pipe_round(len(xs)) batches cycling the rotating sets."""
+    side = [torch.cuda.Stream(stream.device), torch.cuda.Stream(stream.device)]
+    nb = pipe_round(len(xs))
+
+    def run():
+        for sd in side:
+            sd.wait_stream(stream)
+        for i in range(nb):
+            convs[i % 2].dense_forward(xs[i % len(xs)], outs[i % len(outs)], stream=side[i % 2])
+        for sd in side:
+            stream.wait_stream(sd)
+
+    return graph_time_us(torch, stream, run, reps=2) / nb
+
+
 def run_single(args, torch, dev, ws, rank, sc):
     shp = datagen.CONFIGS[args.config]
     n = shp.n
@@ -427,6 +445,8 @@ def run_single(args, torch, dev, ws, rank, sc):
     conv = sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), n, shp.c, shp.h, shp.w,
                          shp.stride, shp.pad, shp.groups)
     lists_per_batch = n * conv.lists(1)["tiles"] * shp.c
+    conv_d2 = sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), n, shp.c, shp.h, shp.w,
+                            shp.stride, shp.pad, shp.groups)  # second dense workspace (dense_two_stream_us)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     stream = torch.cuda.Stream(dev)
     # f3: measured crossover sparsity for this batch (before any capture)
@@ -477,6 +497,7 @@ def run_single(args, torch, dev, ws, rank, sc):
         res["dense_tc_us"] = rotating_time_us(torch, stream, [lambda i=i: conv.dense_forward(xs[i], outs[i],
                                                                                              stream=stream)
                                                               for i in range(nsets)], rot)
+        res["dense_tc_2stream_us"] = dense_two_stream_us(torch, stream, [conv, conv_d2], xs, outs)
         res["compact_warm_us"] = graph_time_us(torch, stream, lambda: conv.compact(xs[0], stream=stream))
         res["gather_warm_us"] = graph_time_us(torch, stream, lambda: conv.gather(n, outs[0], stream=stream))
         res["dense_tc_warm_us"] = graph_time_us(torch, stream,
@@ -603,8 +624,12 @@ def run_ours(args):
         "dense_tc": {"us": round(v["dense_tc_us"], 3), "l2_warm_us": round(v["dense_tc_warm_us"], 3),
                      "gflops": round(gflops(v["dense"], v["dense_tc_us"] / 1e3), 2),
                      "sparse_speedup": round(v["dense_tc_us"] / (v["ms_per_step"] * 1e3), 3),
+                     "two_stream_us": round(v["dense_tc_2stream_us"], 3),
+                     "sparse_speedup_vs_two_stream": round(v["dense_tc_2stream_us"] / (v["ms_per_step"] * 1e3), 3),
                      "note": "in-library tcgen05 TF32 implicit-GEMM conv (dense_conv_forward) on the same batch, "
-                             "same rotating sets (L2-cold) as the sparse step"},
+                             "same rotating sets (L2-cold) as the sparse step; us: back to back on one stream; "
+                             "two_stream_us: per batch with batches alternating between two streams and two plans "
+                             "(the cross-batch overlap the pipelined sparse steps get)"},
         "cudnn_context": {"fp32_us": round(v["cudnn_fp32_us"], 3), "tf32_us": round(v["cudnn_tf32_us"], 3),
                           "note": "torch.nn.functional.conv2d (cuDNN) on the same rotating sets; context only, not "
                                   "part of the library"},
@@ -617,6 +642,7 @@ def run_ours(args):
                                                      / FP32_PEAK_TFLOPS, 4),
                            "gather_us": round(r["gather_us"], 3), "compact_us": round(r["compact_us"], 3),
                            "dense_tc_speedup": round(r["dense_tc_us"] / (r["ms_per_step"] * 1e3), 3),
+                           "dense_tc_two_stream_speedup": round(r["dense_tc_2stream_us"] / (r["ms_per_step"] * 1e3), 3),
                            "auto_us": round(r["auto_us"], 3), "auto_path": r["auto_path"]}
                   for s, r in sweep.items()},
         "crossover": {"s_star": round(conv.s_star_calibrated, 4), "auto_us": round(v["auto_us"], 3),
@@ -895,10 +921,32 @@ def run_table2(args):
                              shp.stride, shp.pad, shp.groups)
         out = torch.empty((shp.n,) + conv.out_shape, device=dev)
         t_s = graph_time_us(torch, stream, lambda: conv.forward(x, out, stream=stream))
+        # a stream of batches through sparse_conv_forward_batches (12 per call; batches b and b+2
+        # share a stage-2 stream, so two output buffers)
+        out2 = torch.empty_like(out)
+        conv.reserve_batches()
+        t_p = graph_time_us(torch, stream, lambda: conv.forward_batches([x] * 12, [out, out2] * 6, stream=stream),
+                            reps=3) / 12
         try:
             t_d = graph_time_us(torch, stream, lambda: conv.dense_forward(x, out, stream=stream), reps=5)
+            # the dense path given the same cross-batch overlap: a second plan (its own channels-last
+            # workspace), batches alternating between two streams
+            conv2 = sc.SparseConv(torch.from_numpy(w).to(dev), torch.from_numpy(b).to(dev), shp.n, shp.c, shp.h,
+                                  shp.w, shp.stride, shp.pad, shp.groups)
+            side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+
+            def dense_2s():
+                for sd in side:
+                    sd.wait_stream(stream)
+                for i in range(12):
+                    (conv, conv2)[i % 2].dense_forward(x, (out, out2)[i % 2], stream=side[i % 2])
+                for sd in side:
+                    stream.wait_stream(sd)
+
+            t_d2 = graph_time_us(torch, stream, dense_2s, reps=3) / 12
+            del conv2
         except sc.SparseConvError:
-            t_d = None
+            t_d = t_d2 = None
         s_star = conv.calibrate_crossover(shp.n, stream)
         t_a = graph_time_us(torch, stream, lambda: conv.forward_auto(x, out, stream=stream), reps=5)
         path = "sparse" if conv.last_path()[0] == sc.SC_PATH_SPARSE else "dense"
@@ -906,8 +954,11 @@ def run_table2(args):
         cpu = PAPER_TABLE3.get(shp.name)
         rows.append({"layer": shp.name, "shape": f"{shp.c}x{shp.h}x{shp.w}->{shp.k} {shp.r}x{shp.s} p{shp.pad} "
                                                  f"t{shp.stride}", "s": s, "variant": conv.variant[1],
-                     "sparse_us": round(t_s, 2), "dense_tc_us": None if t_d is None else round(t_d, 2),
+                     "sparse_us": round(t_s, 2), "sparse_pipelined_us": round(t_p, 2),
+                     "dense_tc_us": None if t_d is None else round(t_d, 2),
                      "b200_speedup_sparse_over_dense": None if t_d is None else round(t_d / t_s, 3),
+                     "dense_tc_2stream_us": None if t_d2 is None else round(t_d2, 2),
+                     "b200_speedup_pipelined": None if t_d2 is None else round(min(t_d, t_d2) / t_p, 3),
                      "s_star": round(s_star, 4), "auto_us": round(t_a, 2), "auto_path": path,
                      "sparse_frac_fp32": round(2 * exact / (t_s * 1e-6) / 1e12 / FP32_PEAK_TFLOPS, 4),
                      "paper_cpu_gemm_ms": cpu[0] if cpu else None, "paper_cpu_isc_ms": cpu[1] if cpu else None,
