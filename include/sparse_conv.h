@@ -246,7 +246,10 @@ sc_status sparse_conv_last_path(sc_plan plan, int32_t *path, int64_t *nnz);
  * are caller-owned outputs, each nullable (not computed), fully overwritten.
  * fp32 accumulation in a fixed order (deterministic).  Stream-ordered, no
  * allocation, graph-capturable; shares the plan's list workspace with the
- * forward (do not overlap the two).  SC_ERR_UNSUPPORTED unless the plan uses
+ * forward (do not overlap the two).  dz and dbias run on a second plan-owned
+ * stream beside dW, forked from and joined into `stream`.  That stream is
+ * created by the first call made outside stream capture; until then the
+ * kernels run on `stream` alone, with the same results.  SC_ERR_UNSUPPORTED unless the plan uses
  * the plane-major stage 1 (H*W <= 1024, H <= 31, <= 32 row tiles) and R x S is
  * 1x1, 3x3 or 5x5. */
 sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float *d_in, const float *d_dout, float *d_dw,

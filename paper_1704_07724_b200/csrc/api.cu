@@ -64,6 +64,9 @@ struct sc_plan_s {
     uint32_t* prow2 = nullptr;
     cudaStream_t bs[3] = {};
     cudaEvent_t bev_fork = nullptr, bev_s1 = nullptr, bev_g[2] = {};
+    // sparse_conv_backward: dgrad + dbias on a second stream beside wgrad (created on first use)
+    cudaStream_t bwd_s2 = nullptr;
+    cudaEvent_t bwd_fork = nullptr, bwd_join = nullptr;
 };
 
 namespace {
@@ -239,8 +242,9 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->prow2);
     for (auto& h : p->bs)
         if (h) cudaStreamDestroy(h);
-    for (cudaEvent_t ev : {p->bev_fork, p->bev_s1, p->bev_g[0], p->bev_g[1]})
+    for (cudaEvent_t ev : {p->bev_fork, p->bev_s1, p->bev_g[0], p->bev_g[1], p->bwd_fork, p->bwd_join})
         if (ev) cudaEventDestroy(ev);
+    if (p->bwd_s2) cudaStreamDestroy(p->bwd_s2);
     delete p;
 }
 
@@ -904,9 +908,21 @@ sc_status sparse_conv_backward(sc_plan plan, int64_t n, const float* d_in, const
         e = sc::launch_plane_lists(plan->g, n, d_in, plan->cnt, plan->plist, plan->prow, s);
         plan->lists_layout = e == cudaSuccess ? 1 : 0;
     }
+    if (e == cudaSuccess && !plan->bwd_s2) {
+        // the second stream and its events are created outside stream capture (under capture the
+        // kernels run on `stream` alone: same results, no overlap)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(s, &cs)) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+            if ((e = cudaStreamCreateWithFlags(&plan->bwd_s2, cudaStreamNonBlocking)) == cudaSuccess &&
+                (e = cudaEventCreateWithFlags(&plan->bwd_fork, cudaEventDisableTiming)) == cudaSuccess)
+                e = cudaEventCreateWithFlags(&plan->bwd_join, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(e, "backward stream setup");
+        }
+    }
     if (e == cudaSuccess)
         e = sc::launch_backward(plan->g, plan->bg, n, plan->plist, plan->prow, d_dout, plan->wpack, plan->bws,
-                                plan->bdt, d_dw, d_dbias, d_dz, s);
+                                plan->bdt, d_dw, d_dbias, d_dz, s, plan->bwd_join ? plan->bwd_s2 : nullptr,
+                                plan->bwd_fork, plan->bwd_join);
     return e == cudaSuccess ? SC_OK : cuda_fail(e, "backward launch");
 }
 

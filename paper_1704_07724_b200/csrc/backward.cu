@@ -560,7 +560,7 @@ void backward_geometry(const Geometry& g, BwdGeom* b) {
 
 cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, const uint2* plist, const uint32_t* prow,
                             const float* dout, const float* wpack, float* ws, float* doutT, float* dw, float* dbias,
-                            float* dz, cudaStream_t st) {
+                            float* dz, cudaStream_t st, cudaStream_t st2, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     using namespace bwd;
     if (!b.supported) return cudaErrorNotSupported;
     Args a;
@@ -585,7 +585,7 @@ cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, cons
                                                                     (int)b.kchunks, howo);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    auto run = [&](bool wgrad) -> cudaError_t {
+    auto run = [&](bool wgrad, cudaStream_t rs) -> cudaError_t {
         const int d = wgrad ? 0 : 1;
         a.BY = (int)b.by[d];
         a.bands = (int)b.bands[d];
@@ -598,31 +598,39 @@ cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, cons
         a.ipc = (int)((n + a.splits - 1) / a.splits);
         const int G = (int)g.G;
         if (g.R == 1) {
-            if (b.kl == 1) return launch_rs<1, 1, 1>(a, G, wgrad, smem, st);
-            if (b.kl == 2) return launch_rs<1, 1, 2>(a, G, wgrad, smem, st);
-            return launch_rs<1, 1, 4>(a, G, wgrad, smem, st);
+            if (b.kl == 1) return launch_rs<1, 1, 1>(a, G, wgrad, smem, rs);
+            if (b.kl == 2) return launch_rs<1, 1, 2>(a, G, wgrad, smem, rs);
+            return launch_rs<1, 1, 4>(a, G, wgrad, smem, rs);
         }
         if (g.R == 3) {
-            if (b.kl == 1) return launch_rs<3, 3, 1>(a, G, wgrad, smem, st);
-            if (b.kl == 2) return launch_rs<3, 3, 2>(a, G, wgrad, smem, st);
-            return launch_rs<3, 3, 4>(a, G, wgrad, smem, st);
+            if (b.kl == 1) return launch_rs<3, 3, 1>(a, G, wgrad, smem, rs);
+            if (b.kl == 2) return launch_rs<3, 3, 2>(a, G, wgrad, smem, rs);
+            return launch_rs<3, 3, 4>(a, G, wgrad, smem, rs);
         }
-        if (b.kl == 1) return launch_rs<5, 5, 1>(a, G, wgrad, smem, st);
-        return launch_rs<5, 5, 2>(a, G, wgrad, smem, st);
+        if (b.kl == 1) return launch_rs<5, 5, 1>(a, G, wgrad, smem, rs);
+        return launch_rs<5, 5, 2>(a, G, wgrad, smem, rs);
     };
+    // dgrad and dbias are independent of wgrad: with a second stream they run beside it (each
+    // kernel's last wave overlaps the other's), joined back into st at the end
+    const bool two = st2 && ev_fork && ev_join && dw && (dz || dbias);
+    cudaStream_t sd = two ? st2 : st;
+    if (two && ((e = cudaEventRecord(ev_fork, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_fork, 0)) != cudaSuccess))
+        return e;
+    if (dz) {  // run() fills the launch-specific fields of `a`; the launch copies them
+        if ((e = run(false, sd)) != cudaSuccess) return e;
+    }
     if (dw) {
-        if ((e = run(true)) != cudaSuccess) return e;
+        if ((e = run(true, st)) != cudaSuccess) return e;
         const int64_t count = g.K * g.Cg * g.R * g.S;
         bwd_reduce_kernel<<<148 * 4, 256, 0, st>>>(ws, a.splits, count, dw);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (dbias) {
-        bwd_dbias_kernel<<<(unsigned)g.K, 256, 0, st>>>(dout, (int)n, (int)g.K, (int)(g.Ho * g.Wo), dbias);
+        bwd_dbias_kernel<<<(unsigned)g.K, 256, 0, sd>>>(dout, (int)n, (int)g.K, (int)(g.Ho * g.Wo), dbias);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (dz) {
-        if ((e = run(false)) != cudaSuccess) return e;
-    }
+    if (two && ((e = cudaEventRecord(ev_join, st2)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess))
+        return e;
     return cudaSuccess;
 }
 

@@ -112,7 +112,8 @@ cudaError_t launch_synth_relu(float* x, int64_t elems, double rho, uint32_t seed
 void backward_geometry(const Geometry& g, BwdGeom* b);
 cudaError_t launch_backward(const Geometry& g, const BwdGeom& b, int64_t n, const uint2* plist, const uint32_t* prow,
                             const float* dout, const float* wpack, float* ws, float* doutT, float* dw, float* dbias,
-                            float* dz, cudaStream_t st);
+                            float* dz, cudaStream_t st, cudaStream_t st2 = nullptr, cudaEvent_t ev_fork = nullptr,
+                            cudaEvent_t ev_join = nullptr);
 
 // Run-time specialised stage 2 (jit.cu): a gather variant generated for the plan's
 // shape and compiled through NVRTC when no generated variant matches.
