@@ -349,9 +349,10 @@ JIT_TILINGS = {1: "7,2,7,1,8,4,3,254", 2: "3,2,7,1,8,4,3,254", 3: "2,2,7,1,4,4,3
                5: "6,2,7,1,4,4,3,254", 28: "1,4,11,1,16,2,3,254", 29: "4,1,11,1,16,2,3,254",
                7: "7,1,11,1,16,4,3,254", 10: "3,3,11,1,8,4,3,254", 11: "3,4,7,1,8,3,3,254",
                12: "2,4,11,1,8,3,3,254", 13: "5,2,11,1,8,4,3,254", 14: "1,4,11,1,8,3,3,254",
-               30: "2,1,11,1,16,2,3,254", 48: "3,3,11,1,16,2,2,254", 49: "2,4,11,1,16,3,3,510"}
+               30: "2,1,11,1,16,2,3,254", 48: "3,3,11,1,16,2,2,254", 49: "2,4,11,1,16,3,3,510",
+               50: "1,1,4,1,10,2,3,254"}
 FORCED = ([("C2", v) for v in (0, 1, 7, 10, 11, 12, 13, 21)] + [("C4a", v) for v in (0, 2, 14, 28, 51)] +
-          [("C4b", v) for v in (0, 4, 29, 30, 52)] + [("C3", v) for v in (0, 3, 33)] + [("C1", v) for v in (0, 5, 50)])
+          [("C4b", v) for v in (0, 4, 29, 30, 52)] + [("C3", v) for v in (0, 3, 33)] + [("C1", v) for v in (0, 5, 50, 57)])
 
 
 def force_kernel(monkeypatch, variant):

@@ -44,7 +44,7 @@ VARIANTS = [
     (33, "r5s5p2_w27_ty3_kl1_nw11", 5, 5, 2, 27, 3, 1, 11, 1, 16, 2),        # C3: x-pairs
     # round 2: best of whole-forward sweeps (stage 1 depends on the tile height too;
     # profiles/r2_jit_tune_*.txt), replacing V5 / V28 / V29
-    (50, "r5s5p0_w12_ty1_kl1_nw4_ch10", 5, 5, 0, 12, 1, 1, 4, 1, 10, 2),     # C1: x-pairs, 4 warps per CTA
+    (57, "r5s5p0_w12_ty1_kl1_nw7_ch10", 5, 5, 0, 12, 1, 1, 7, 1, 10, 2),     # C1: x-pairs, 7 warps (pipelined batches)
     (51, "r3s3p1_w28_ty2_kl2_nw11_ch32", 3, 3, 1, 28, 2, 2, 11, 1, 32, 2),   # C4a: k-pairs
     (52, "r5s5p2_w28_ty3_kl1_nw11", 5, 5, 2, 28, 3, 1, 11, 1, 16, 2),        # C4b: x-pairs
     # paper Table 2 shapes: stride 2, 1x1, small planes
@@ -72,6 +72,8 @@ VARIANTS = [
 # into libsparseconv.so; any of them can be generated at run time for tuning or tests with
 # SC_JIT_FORCE="TY,KL,NW,MINB,CH,STAGES,SLOTS,PIECE" (csrc/jit.cu).
 SUPERSEDED = [
+    (50, "r5s5p0_w12_ty1_kl1_nw4_ch10", 5, 5, 0, 12, 1, 1, 4, 1, 10, 2),     # C1 until late round 2 (equal single
+                                                                               # batch, 8% slower pipelined)
     (48, "r1s1p0_w14_ty3_kl3_sl2_k150", 1, 1, 0, 14, 3, 3, 11, 1, 16, 2, None, 2, 254, 1, 150),  # Inception4a.1 until round 2
     (49, "r1s1p0_w7_ty2_kl4_s3p510_k200", 1, 1, 0, 7, 2, 4, 11, 1, 16, 3, None, 3, 510, 1, 200),  # Inception5a.1 until round 2
     (5, "r5s5p0_w12_ty6_kl2", 5, 5, 0, 12, 6, 2, 7, 1, 4, 4),      # C1 until round 2
@@ -95,7 +97,7 @@ ABLATIONS = [
 ]
 
 # selection order = first match wins (measured fastest first)
-PRIORITY = [21, 51, 52, 33, 50, 53, 54, 55, 56]  # 53-56: Kg >= KMIN and KL = wide_1x1_kl
+PRIORITY = [21, 51, 52, 33, 57, 53, 54, 55, 56]  # 53-56: Kg >= KMIN and KL = wide_1x1_kl
 
 
 def gen_variant(vid, name, R, S, P, W, TY, KL, NW, MINB, CH, STAGES, ablate=None, SLOTS=3, PIECE=254, T=1, KMIN=0):
