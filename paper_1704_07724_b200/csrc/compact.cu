@@ -234,7 +234,7 @@ constexpr int kMaxTiles = 32;     // tiles per image on the plane-major path
 }  // namespace
 
 template <int NSLOT, int IMG>
-__global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
+__global__ void __launch_bounds__(kPlaneWarps * 32, NSLOT >= 16 ? 4 : 0) compact_plane_count_kernel(
     const float* __restrict__ in, int nimg, int C, int H, int W, int TYT, int P, int NWR, int tiles,
     uint32_t* __restrict__ cnt, uint2* __restrict__ plist, uint32_t* __restrict__ prow, Gate gate) {
     // the emit kernel (a programmatic dependent on the forward path) may be scheduled once every
@@ -267,33 +267,29 @@ __global__ void __launch_bounds__(kPlaneWarps * 32) compact_plane_count_kernel(
     float (&v)[NSLOT] = vv[i];
     const unsigned lt = (1u << lane) - 1u;
     uint2* lst = plist + (int64_t)plane * HW;
-    unsigned bal[NSLOT];
-    uint32_t pc[NSLOT];
+    // lane r <= H: nonzeros before element r*W (the first element of row r), accumulated slot by
+    // slot (branch-free: slots below sb whole, slot sb below element eb) so no slot's ballot
+    // stays live past its own iteration
+    const int eb = lane * W;
+    const int sb = eb >> 5;
+    const unsigned mb = (1u << (eb & 31)) - 1u;
+    uint32_t pre = 0;
     uint32_t total = 0;
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u) {
         const bool nz = v[u] != 0.0f;  // IEEE: -0.0 is zero
-        bal[u] = __ballot_sync(0xffffffffu, nz);
-        pc[u] = __popc(bal[u]);
-        if (bal[u] != 0u) {  // warp-uniform: slots without a nonzero store nothing
+        const unsigned bal = __ballot_sync(0xffffffffu, nz);
+        if (bal != 0u) {  // warp-uniform: slots without a nonzero store nothing
             // predicated store (no branch / reconvergence per lane)
-            const uint2* dst = lst + total + __popc(bal[u] & lt);
+            const uint2* dst = lst + total + __popc(bal & lt);
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.global.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(dst),
                 "r"(__float_as_uint(v[u])), "r"(32u * u + lane), "r"((unsigned)nz)
                 : "memory");
         }
-        total += pc[u];
-    }
-    // lane r <= H: nonzeros before element r*W (the first element of row r)
-    const int eb = lane * W;
-    const int sb = eb >> 5;
-    const unsigned mb = (1u << (eb & 31)) - 1u;
-    uint32_t pre = 0;
-#pragma unroll
-    for (int u = 0; u < NSLOT; ++u) {  // branch-free: slots below sb whole, slot sb below element eb
         const unsigned m = u < sb ? 0xffffffffu : (u == sb ? mb : 0u);
-        pre += __popc(bal[u] & m);
+        pre += __popc(bal & m);
+        total += __popc(bal);
     }
     if (lane > H) pre = total;
     if (lane <= H) prow[(int64_t)plane * (H + 1) + lane] = pre;

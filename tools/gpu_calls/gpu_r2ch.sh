@@ -1,0 +1,2 @@
+timeout 1500 python -m pytest tests/test_gpu_sparse.py -q -x -k "full_config or small_batch" > gpurun_out/t_cnt5.log 2>&1; echo "pytest=$?"
+for c in C4a C3 C2 C4b; do timeout 900 python bench.py --config $c --no-sweep --no-cpu-baseline > gpurun_out/bench_cnt5_$c.jsonl 2> gpurun_out/bench_cnt5_$c.err; echo "bench $c=$?"; done
