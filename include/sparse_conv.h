@@ -167,6 +167,18 @@ sc_status dense_conv_forward(sc_plan plan, int64_t n, const float *d_in, float *
 sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float *h_in, float *h_out,
                                    sc_stream_t stream);
 
+/* End to end for a sequence of nbatch independent batches of n images: h_in[b] / h_out[b]
+ * (host arrays of nbatch host pointers, each buffer as in sparse_conv_forward_host) hold batch
+ * b.  Same chunked pipeline as sparse_conv_forward_host, continued across batches: batch b+1's
+ * copy-in and kernels run while batch b's copy-out is still in flight.  The two copy directions
+ * use separate copy engines, so the sequence runs at the PCIe rate rather than the sum of the
+ * legs.  The plan keeps two device staging sets and alternates between them.  Every batch's
+ * output is identical to sparse_conv_forward_host on that batch.  Starts after the work
+ * queued on `stream`, synchronizes `stream` before returning; nbatch == 1 is exactly
+ * sparse_conv_forward_host.  h_in / h_out should be pinned. */
+sc_status sparse_conv_forward_host_batches(sc_plan plan, int32_t nbatch, int64_t n, const float *const *h_in,
+                                           float *const *h_out, sc_stream_t stream);
+
 /* A chain of layers (e.g. C5: conv3 -> ReLU -> conv4 -> ReLU -> conv5, the
  * ReLUs fused via SC_FLAG_FUSE_RELU) on the first n images: plans[l+1]'s input
  * is plans[l]'s output (K, H_out, W_out must match C, H, W).  d_in is layer

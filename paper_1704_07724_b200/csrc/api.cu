@@ -55,6 +55,11 @@ struct sc_plan_s {
     static constexpr int kHostComp = 4;  // compute streams (chunks use disjoint workspace slices)
     cudaStream_t hs[2 + kHostComp] = {};  // [0] copy-in, [1] copy-out, [2..] compute
     cudaEvent_t ev_in[kHostChunks] = {}, ev_comp[kHostChunks] = {}, ev_start = nullptr, ev_done = nullptr;
+    // sparse_conv_forward_host_batches: a second staging set and, per set and chunk, copy-in /
+    // kernels / copy-out events (created on first use)
+    float* stage_in2 = nullptr;
+    float* stage_out2 = nullptr;
+    cudaEvent_t hb_in[2][kHostChunks] = {}, hb_comp[2][kHostChunks] = {}, hb_out[2][kHostChunks] = {};
     // sparse_conv_forward_batches (sparse_conv_reserve_batches): a second stage-1 workspace, a
     // low-priority stage-1 stream [0] and two high-priority stage-2 streams [1], [2]
     uint2* entries2 = nullptr;
@@ -224,6 +229,12 @@ void free_plan(sc_plan_s* p) {
     cudaFree(p->prow);
     cudaFree(p->stage_in);
     cudaFree(p->stage_out);
+    cudaFree(p->stage_in2);
+    cudaFree(p->stage_out2);
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < sc_plan_s::kHostChunks; ++i)
+            for (cudaEvent_t ev : {p->hb_in[k][i], p->hb_comp[k][i], p->hb_out[k][i]})
+                if (ev) cudaEventDestroy(ev);
     cudaFree(p->sel);
     for (auto& h : p->hs)
         if (h) cudaStreamDestroy(h);
@@ -336,6 +347,45 @@ cudaError_t ensure_batches(sc_plan_s* p) {
     for (cudaEvent_t* ev : {&p->bev_fork, &p->bev_s1, &p->bev_g[0], &p->bev_g[1]})
         if (!*ev && (e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
     return cudaDeviceSynchronize();  // the workspace memset
+}
+
+// sparse_conv_forward_host(_batches): compute streams (SC_HOST_STREAMS, 1..kHostComp, default 2)
+int host_comp_streams() {
+    static const int ncomp = [] {
+        const char* v = getenv("SC_HOST_STREAMS");  // measurement knob
+        const int c = v ? atoi(v) : 2;
+        return c < 1 ? 1 : (c > sc_plan_s::kHostComp ? sc_plan_s::kHostComp : c);
+    }();
+    return ncomp;
+}
+
+// Chunks of whole images for the host paths, boundaries at multiples of 4 images (16-byte
+// aligned device pointers for any shape): a small first chunk starts the copy-out early (the
+// copy-out of the dense fp32 output is the longest leg), the rest split evenly.  Returns the
+// chunk count; bounds[0..chunks].  SC_HOST_CHUNKS / SC_HOST_FIRST: measurement knobs.
+int host_chunk_bounds(int64_t n, int64_t* bounds) {
+    static const int max_chunks = [] {
+        const char* v = getenv("SC_HOST_CHUNKS");
+        const int c = v ? atoi(v) : 8;
+        return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
+    }();
+    static const int64_t first_env = [] {
+        const char* v = getenv("SC_HOST_FIRST");  // images in the first chunk (0: even split)
+        return (int64_t)(v ? atoi(v) : -1);
+    }();
+    int chunks = (int)(n / 4 < max_chunks ? n / 4 : max_chunks);
+    if (chunks < 1) chunks = 1;
+    bounds[0] = 0;
+    int64_t first = first_env >= 0 ? first_env : n / 8;
+    first = (first + 3) & ~(int64_t)3;
+    if (chunks == 1 || first <= 0 || first >= n) {
+        for (int i = 1; i <= chunks; ++i) bounds[i] = i == chunks ? n : ((n * i / chunks) & ~(int64_t)3);
+    } else {
+        bounds[1] = first;
+        for (int i = 2; i <= chunks; ++i)
+            bounds[i] = i == chunks ? n : ((first + (n - first) * (i - 1) / (chunks - 1)) & ~(int64_t)3);
+    }
+    return chunks;
 }
 
 // Best-of-3 device time (us) of one path on the staged input (one untimed run first).
@@ -659,39 +709,10 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
         return cuda_fail(e, "host pipeline setup");
     cudaStream_t s = (cudaStream_t)stream;
     cudaStream_t h2d = plan->hs[0], d2h = plan->hs[1];
-    static const int ncomp = [] {
-        const char* v = getenv("SC_HOST_STREAMS");  // measurement knob: compute streams, 1..kHostComp
-        const int c = v ? atoi(v) : 2;
-        return c < 1 ? 1 : (c > sc_plan_s::kHostComp ? sc_plan_s::kHostComp : c);
-    }();
+    const int ncomp = host_comp_streams();
     const int64_t in_img = g.C * g.H * g.W, out_img = g.K * g.Ho * g.Wo;
-    // chunks of whole images, boundaries at multiples of 4 images (16-byte aligned device
-    // pointers for any shape); copy-in, kernels and copy-out of different chunks overlap (separate
-    // copy engines for the two directions, kernels of consecutive chunks on different streams)
-    static const int max_chunks = [] {
-        const char* v = getenv("SC_HOST_CHUNKS");  // measurement knob, 1..kHostChunks
-        const int c = v ? atoi(v) : 8;
-        return c < 1 ? 1 : (c > sc_plan_s::kHostChunks ? sc_plan_s::kHostChunks : c);
-    }();
-    static const int64_t first_env = [] {
-        const char* v = getenv("SC_HOST_FIRST");  // measurement knob: images in the first chunk (0: even split)
-        return (int64_t)(v ? atoi(v) : -1);
-    }();
-    int chunks = (int)(n / 4 < max_chunks ? n / 4 : max_chunks);
-    if (chunks < 1) chunks = 1;
-    // chunk boundaries (multiples of 4 images): a small first chunk starts the copy-out early
-    // (the copy-out of the dense fp32 output is the longest leg), the rest split evenly
     int64_t bounds[sc_plan_s::kHostChunks + 1];
-    bounds[0] = 0;
-    int64_t first = first_env >= 0 ? first_env : n / 8;
-    first = (first + 3) & ~(int64_t)3;
-    if (chunks == 1 || first <= 0 || first >= n) {
-        for (int i = 1; i <= chunks; ++i) bounds[i] = i == chunks ? n : ((n * i / chunks) & ~(int64_t)3);
-    } else {
-        bounds[1] = first;
-        for (int i = 2; i <= chunks; ++i)
-            bounds[i] = i == chunks ? n : ((first + (n - first) * (i - 1) / (chunks - 1)) & ~(int64_t)3);
-    }
+    const int chunks = host_chunk_bounds(n, bounds);
     if ((e = cudaEventRecord(plan->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
     for (int k = 0; k < 2 + ncomp; ++k)
         if ((e = cudaStreamWaitEvent(plan->hs[k], plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
@@ -716,6 +737,77 @@ sc_status sparse_conv_forward_host(sc_plan plan, int64_t n, const float* h_in, f
     }
     // the caller's stream resumes after everything (kernels and copies) of this call
     // (every chunk's kernels precede its copy-out, so the copy-out stream joins them all)
+    if ((e = cudaEventRecord(plan->ev_done, d2h)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, plan->ev_done, 0)) != cudaSuccess)
+        return cuda_fail(e, "stream join");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+    return SC_OK;
+}
+
+sc_status sparse_conv_forward_host_batches(sc_plan plan, int32_t nbatch, int64_t n, const float* const* h_in,
+                                           float* const* h_out, sc_stream_t stream) {
+    sc_status st = check_forward(plan, n);
+    if (st != SC_OK) return st;
+    if (nbatch < 1 || !h_in || !h_out)
+        return fail(SC_ERR_INVALID_ARGUMENT, "nbatch=%d: need nbatch >= 1 and the h_in / h_out arrays", (int)nbatch);
+    for (int32_t b = 0; b < nbatch; ++b)
+        if (!h_in[b] || !h_out[b]) return fail(SC_ERR_INVALID_ARGUMENT, "host buffer of batch %d is NULL", (int)b);
+    if (nbatch == 1) return sparse_conv_forward_host(plan, n, h_in[0], h_out[0], stream);
+    DeviceGuard guard(plan->device);
+    const Geometry& g = plan->g;
+    cudaError_t e;
+    if ((e = ensure_staging(plan)) != cudaSuccess || (e = ensure_host_pipeline(plan)) != cudaSuccess)
+        return cuda_fail(e, "host pipeline setup");
+    if ((!plan->stage_in2 && (e = cudaMalloc(&plan->stage_in2, sizeof(float) * g.N * g.C * g.H * g.W)) != cudaSuccess) ||
+        (!plan->stage_out2 &&
+         (e = cudaMalloc(&plan->stage_out2, sizeof(float) * g.N * g.K * g.Ho * g.Wo)) != cudaSuccess))
+        return cuda_fail(e, "host staging");
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < sc_plan_s::kHostChunks; ++i)
+            for (cudaEvent_t* ev : {&plan->hb_in[k][i], &plan->hb_comp[k][i], &plan->hb_out[k][i]})
+                if (!*ev && (e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_fail(e, "host events");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStream_t h2d = plan->hs[0], d2h = plan->hs[1];
+    const int ncomp = host_comp_streams();
+    const int64_t in_img = g.C * g.H * g.W, out_img = g.K * g.Ho * g.Wo;
+    int64_t bounds[sc_plan_s::kHostChunks + 1];
+    const int chunks = host_chunk_bounds(n, bounds);
+    if ((e = cudaEventRecord(plan->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    for (int k = 0; k < 2 + ncomp; ++k)
+        if ((e = cudaStreamWaitEvent(plan->hs[k], plan->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    for (int32_t b = 0; b < nbatch; ++b) {
+        // batch b uses staging set b & 1; chunk i of every batch uses workspace slice i on compute
+        // stream 2 + i % ncomp (so batch b's chunk i follows batch b-1's in stream order)
+        const int set = b & 1;
+        float* sin = set ? plan->stage_in2 : plan->stage_in;
+        float* sout = set ? plan->stage_out2 : plan->stage_out;
+        for (int i = 0; i < chunks; ++i) {
+            const int64_t c0 = bounds[i], c1 = bounds[i + 1];
+            if (c1 <= c0) continue;
+            const size_t bi = sizeof(float) * (c1 - c0) * in_img, bo = sizeof(float) * (c1 - c0) * out_img;
+            float* din = sin + c0 * in_img;
+            float* dout = sout + c0 * out_img;
+            cudaStream_t comp = plan->hs[2 + i % ncomp];
+            // the copy-in overwrites what batch b-2's kernels read; the kernels overwrite what batch
+            // b-2's copy-out read
+            if (b >= 2 && (e = cudaStreamWaitEvent(h2d, plan->hb_comp[set][i], 0)) != cudaSuccess)
+                return cuda_fail(e, "stream wait");
+            if ((e = cudaMemcpyAsync(din, h_in[b] + c0 * in_img, bi, cudaMemcpyHostToDevice, h2d)) != cudaSuccess ||
+                (e = cudaEventRecord(plan->hb_in[set][i], h2d)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(comp, plan->hb_in[set][i], 0)) != cudaSuccess)
+                return cuda_fail(e, "H2D copy");
+            if (b >= 2 && (e = cudaStreamWaitEvent(comp, plan->hb_out[set][i], 0)) != cudaSuccess)
+                return cuda_fail(e, "stream wait");
+            if ((e = enqueue_sparse(plan, c1 - c0, din, dout, comp, {}, c0)) != cudaSuccess)
+                return cuda_fail(e, "forward");
+            if ((e = cudaEventRecord(plan->hb_comp[set][i], comp)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(d2h, plan->hb_comp[set][i], 0)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(h_out[b] + c0 * out_img, dout, bo, cudaMemcpyDeviceToHost, d2h)) != cudaSuccess ||
+                (e = cudaEventRecord(plan->hb_out[set][i], d2h)) != cudaSuccess)
+                return cuda_fail(e, "D2H copy");
+        }
+    }
     if ((e = cudaEventRecord(plan->ev_done, d2h)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(s, plan->ev_done, 0)) != cudaSuccess)
         return cuda_fail(e, "stream join");

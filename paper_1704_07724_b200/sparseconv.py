@@ -25,7 +25,8 @@ EXPORTS = ("sparse_conv_output_shape", "sparse_conv_create", "sparse_conv_forwar
            "sparse_conv_launch_count", "sc_probe_fma", "sc_flush_l2", "sparse_conv_forward_chain",
            "sparse_conv_forward_auto", "sparse_conv_calibrate_crossover", "sparse_conv_set_crossover",
            "sparse_conv_get_crossover", "sparse_conv_last_path", "sparse_conv_backward", "sc_jit_variant_source",
-           "sc_jit_available", "sparse_conv_plane_lists", "sparse_conv_forward_batches", "sparse_conv_reserve_batches")
+           "sc_jit_available", "sparse_conv_plane_lists", "sparse_conv_forward_batches", "sparse_conv_reserve_batches",
+           "sparse_conv_forward_host_batches")
 SC_PATH_SPARSE, SC_PATH_DENSE = 0, 1
 
 
@@ -72,6 +73,8 @@ def lib():
         L.sparse_conv_gather.argtypes = [vp, i64, vp, vp]
         L.sparse_conv_forward_batches.argtypes = [vp, ctypes.c_int32, i64, ctypes.POINTER(vp), ctypes.POINTER(vp), vp]
         L.sparse_conv_reserve_batches.argtypes = [vp]
+        L.sparse_conv_forward_host_batches.argtypes = [vp, ctypes.c_int32, i64, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                                       vp]
         L.sparse_conv_destroy.argtypes = [vp]
         L.sparse_conv_lists.argtypes = [vp, ctypes.POINTER(ListsView)]
         L.sparse_conv_kernel_variant.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_char_p)]
@@ -260,6 +263,24 @@ class SparseConv:
         _check(lib().sparse_conv_forward_host(self._plan, n, ctypes.c_void_p(h_in.data_ptr()),
                                               ctypes.c_void_p(h_out.data_ptr()), _stream_handle(stream)))
         return h_out
+
+    def forward_host_batches(self, h_ins, h_outs, stream=None):
+        """sparse_conv_forward_host_batches: host batches h_ins[b] -> h_outs[b] (CPU tensors,
+        pinned for full bandwidth), copies and kernels of consecutive batches overlapped;
+        synchronous."""
+        if len(h_ins) != len(h_outs) or not h_ins:
+            raise ValueError("h_ins and h_outs must be non-empty and of equal length")
+        n = h_ins[0].shape[0]
+        for hi, ho in zip(h_ins, h_outs):
+            if hi.device.type != "cpu" or ho.device.type != "cpu" or hi.dtype != torch.float32 or \
+                    ho.dtype != torch.float32 or not hi.is_contiguous() or not ho.is_contiguous():
+                raise ValueError("host batches must be contiguous float32 CPU tensors")
+            if tuple(hi.shape) != (n,) + self.in_shape or tuple(ho.shape) != (n,) + self.out_shape:
+                raise ValueError("host batch shape mismatch")
+        ins = (ctypes.c_void_p * len(h_ins))(*[t.data_ptr() for t in h_ins])
+        ous = (ctypes.c_void_p * len(h_outs))(*[t.data_ptr() for t in h_outs])
+        _check(lib().sparse_conv_forward_host_batches(self._plan, len(h_ins), n, ins, ous, _stream_handle(stream)))
+        return h_outs
 
     # -- test hooks --------------------------------------------------------
     def compact(self, x, stream=None):

@@ -146,3 +146,36 @@ def test_batches_bad_arguments(sc):
     with pytest.raises(sc.SparseConvError) as e:
         sc._check(sc.lib().sparse_conv_forward_batches(conv._plan, 2, 2, ins, ous, None))
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("cfg,n,nbatch", [("C2", 128, 5), ("C4b", 7, 4), ("C1", 9, 3), ("C2", 6, 1)])
+def test_host_batches_match_device_forward(sc, cfg, n, nbatch):
+    """sparse_conv_forward_host_batches: pinned host batches through the chunked copy/compute
+    pipeline continued across batches (two staging sets); every batch's host output equals the
+    device forward of that batch bit for bit (same kernels), the first and last images of the
+    first and last batches against the oracle."""
+    shp = datagen.CONFIGS[cfg]
+    conv, w, b = make(sc, shp, max_batch=max(n, 8))
+    xs = [torch.from_numpy(datagen.activations(shp.with_batch(n), 0.9, seed=200 + i)) for i in range(nbatch)]
+    h_in = [x.pin_memory() for x in xs]
+    h_out = [torch.empty((n,) + conv.out_shape).pin_memory() for _ in range(nbatch)]
+    conv.forward_host_batches(h_in, h_out)
+    for i, (x, o) in enumerate(zip(xs, h_out)):
+        assert torch.equal(o, conv.forward(x.to(DEV)).cpu()), f"batch {i}"
+    for i in sorted({0, nbatch - 1}):
+        check_oracle(h_out[i], xs[i], w, b, shp, [0, n - 1])
+
+
+def test_host_batches_bad_arguments(sc):
+    import ctypes
+    shp = datagen.CONFIGS["C4b"].with_batch(2)
+    conv, _, _ = make(sc, shp)
+    with pytest.raises(sc.SparseConvError) as e:
+        sc._check(sc.lib().sparse_conv_forward_host_batches(conv._plan, 0, 2, None, None, None))
+    assert e.value.status == 1
+    h = torch.zeros((2,) + conv.in_shape)
+    ins = (ctypes.c_void_p * 2)(h.data_ptr(), 0)
+    ous = (ctypes.c_void_p * 2)(h.data_ptr(), h.data_ptr())
+    with pytest.raises(sc.SparseConvError) as e:
+        sc._check(sc.lib().sparse_conv_forward_host_batches(conv._plan, 2, 2, ins, ous, None))
+    assert e.value.status == 1
