@@ -3,7 +3,8 @@ tests/test_gpu_fuzz.py -- more seeds, larger channel and filter counts, batches
 that make multi-wave stage-2 grids -- each checked like the fuzz test: stage-1
 lists bit-exact against the oracle, streams against the test-side adapter,
 sparse outputs within 1e-5*mass + 1e-6, integer data bit-exact.
-Usage: python tools/fuzz_sweep.py [seeds] [shapes per seed] [first seed]"""
+Usage: python tools/fuzz_sweep.py [seeds] [shapes per seed] [first seed] [wide]
+("wide": a quarter of the shapes are 1x1 layers with 150-520 filters per group)"""
 import os
 import sys
 
@@ -18,6 +19,7 @@ from lists_check import check_plane_lists, check_streams  # noqa: E402
 from paper_1704_07724_b200 import datagen, sparseconv as sc  # noqa: E402
 
 DEV = torch.device("cuda:0")
+WIDE = len(sys.argv) > 4 and sys.argv[4] == "wide"
 
 
 def shapes(seed, count):
@@ -33,6 +35,10 @@ def shapes(seed, count):
         r = int(rng.integers(1, min(7, h + 2 * pad) + 1))
         s = int(rng.integers(1, min(7, w + 2 * pad) + 1))
         n = int(rng.choice([1, 3, 8, 40]))
+        if WIDE and rng.random() < 0.25:  # 1x1 with many filters: the KL = 6 / 8 rule (sc_internal.h wide_1x1_kl)
+            r = s = stride = 1
+            pad = 0
+            k = groups * int(rng.integers(150, 521))
         out.append(datagen.ConvShape(f"sweep{seed}_{i}", 2000 + 100 * seed + i, n, c, h, w, k, r, s, stride, pad,
                                      groups))
     return out
