@@ -83,7 +83,7 @@ cudaError_t launch_v(const Geometry& g, int64_t n, const uint2* entries, const u
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;
-    a.edge_last = grid >= 2LL * sm_count() * V::MINB ? 1 : 0;
+    a.edge_last = edge_last_order(grid >= 2LL * sm_count() * V::MINB);
     if (gate.flag != nullptr) {
         if (rowlist != nullptr) return cudaErrorNotSupported;
         auto kg = gather_fast_kernel<V, false, ArgsGated>;

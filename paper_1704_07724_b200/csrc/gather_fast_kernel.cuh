@@ -151,9 +151,10 @@ __global__ void __launch_bounds__((V::NW + 1) * 32, V::MINB) gather_fast_kernel(
     // its last tile.  The edge tiles' input windows are clipped by the padding (C2: 3 and 2 of 4
     // window rows), so their streams are shorter; consecutive units share a CTA whose
     // warps walk the weight ring in lock step, so grouping by tile position keeps short
-    // streams from idling in CTAs of long ones, and the short CTAs run last (measured: C5 -7%,
-    // C2 (1.66 waves) +2%, hence only for grids of >= 2 waves).  A relabelling only: every
-    // stream is computed the same way by whichever warp owns it.
+    // streams from idling in CTAs of long ones, and the short CTAs run last (measured: C5 -7%;
+    // single-batch C2 (1.66 waves) +1%, but -4% per batch when batches are pipelined, so it is
+    // on for every grid: sc_internal.h edge_last_order).  A relabelling only: every stream is
+    // computed the same way by whichever warp owns it.
     int n, tile;
     {
         const int nimg = a.n, T = a.ytiles;

@@ -506,7 +506,7 @@ cudaError_t launch(void* fn, size_t smem, const Params& p, const Geometry& g, in
         int d = 0, sms = 148;
         if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
             sms = 148;
-        a.edge_last = (int64_t)a.ctas_per_kb * g.G * g.kblocks >= 2LL * sms * p.MINB ? 1 : 0;
+        a.edge_last = edge_last_order((int64_t)a.ctas_per_kb * g.G * g.kblocks >= 2LL * sms * p.MINB);
     }
     ag.gate = gate;
     const int64_t grid = (int64_t)a.ctas_per_kb * g.G * g.kblocks;

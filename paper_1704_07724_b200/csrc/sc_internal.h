@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "sc_device.h"
 #include "sparse_conv.h"
@@ -28,6 +29,20 @@ struct Geometry {
 // filters -- KL = the fewest k-blocks among 4, 6, 8 (ties to the narrower) whose one-row tile
 // (Wo*KL accumulators + KL weights) fits V21's 140 registers.  0: not such a layer.  Both the
 // shipped variants V53-V56 (gather_fast.cu) and run-time generated tilings (jit.cu) follow it.
+// Stage-2 unit order (gather_fast_kernel.cuh): interior row tiles first, edge tiles last, so a
+// CTA's warps hold streams of similar length.  Round 1 used it for grids of >= 2 waves only
+// (single-batch C2, 1.66 waves: +1%); with batches pipelined (sparse_conv_forward_batches) the
+// last wave's holes are filled anyway and the balance inside CTAs wins on every grid: C2 158.2 ->
+// 152.0 us per batch, C4b 23.5 -> 22.4 (profiles/r2_edge_last_pipelined.txt).  SC_EDGE_LAST
+// (measurement knob): 0 = grids of >= 2 waves only, as in round 1.
+inline int edge_last_order(bool multi_wave) {
+    static const int force = [] {
+        const char* v = getenv("SC_EDGE_LAST");
+        return v ? atoi(v) : 1;
+    }();
+    return force ? 1 : (multi_wave ? 1 : 0);
+}
+
 inline int wide_1x1_kl(const Geometry& g) {
     if (g.R != 1 || g.S != 1 || g.T != 1 || g.Kg < 150) return 0;
     auto blocks = [&](int64_t k) { return (g.Kg + 32 * k - 1) / (32 * k); };
