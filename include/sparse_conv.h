@@ -136,6 +136,8 @@ sc_status sparse_conv_forward(sc_plan plan, int64_t n, const float *d_in, float 
  * must not be made while `stream` is capturing (SC_ERR_INVALID_ARGUMENT);
  * sparse_conv_reserve_batches does that ahead of time.  nbatch == 1 is exactly
  * sparse_conv_forward.  The same plan must not run another forward concurrently.
+ * Afterwards the list views (sparse_conv_lists / sparse_conv_plane_lists) describe no
+ * batch; they describe the last sparse_conv_forward / sparse_conv_compact only.
  * Why: a stage-2 CTA holds a whole SM
  * (registers and shared memory), and C2 needs 1.66 waves of them. */
 sc_status sparse_conv_forward_batches(sc_plan plan, int32_t nbatch, int64_t n, const float *const *d_in,
@@ -197,8 +199,8 @@ sc_status sparse_conv_forward_host_batches(sc_plan plan, int32_t nbatch, int64_t
  * chunks use two streams owned by plans[0], so one chunk's last, partly filled
  * stage-2 wave of a layer overlaps the other chunk's work. The
  * SC_CHAIN_CHUNKS env var (measurement knob, 1-8) changes the count. The first
- * chunked call creates those streams, so it must not be made while `stream` is
- * capturing (SC_ERR_INVALID_ARGUMENT). */
+ * chunked call made outside stream capture creates those streams; until then the
+ * chain runs unchunked on `stream`, with the same results. */
 sc_status sparse_conv_forward_chain(const sc_plan *plans, int32_t nplans, int64_t n, const float *d_in,
                                     float *const *d_outs, sc_stream_t stream);
 

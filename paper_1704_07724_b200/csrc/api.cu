@@ -850,11 +850,11 @@ sc_status sparse_conv_forward_chain(const sc_plan* plans, int32_t nplans, int64_
     sc_plan_s* p0 = plans[0];
     cudaError_t e;
     if (!p0->hs[2] || !p0->hs[3] || !p0->ev_start || !p0->ev_comp[chunks - 1]) {
+        // the streams are created outside stream capture only; a first call under capture runs the
+        // chain unchunked on `stream` (same results)
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
-        if (cs != cudaStreamCaptureStatusNone)
-            return fail(SC_ERR_INVALID_ARGUMENT, "first chunked sparse_conv_forward_chain under stream capture: run it "
-                                                 "once outside capture (creates the plan's streams)");
+        if (cs != cudaStreamCaptureStatusNone) return enqueue_chain(plans, nplans, n, 0, d_in, d_outs, s);
         if ((e = ensure_host_pipeline(p0)) != cudaSuccess) return cuda_fail(e, "chain streams");
     }
     if ((e = cudaEventRecord(p0->ev_start, s)) != cudaSuccess) return cuda_fail(e, "event record");

@@ -102,3 +102,31 @@ def test_chain_fused_lists_match_compaction_and_oracle(n):
     sc.chain_forward(convs, x, [None] * (len(convs) - 1) + [fin])
     torch.cuda.synchronize()
     assert torch.equal(fin, outs[-1])
+
+
+def test_chunked_chain_first_call_under_capture():
+    """n >= 256 runs the chain in two image chunks on plan-owned streams, created on the first call
+    made outside stream capture; a first call under capture runs unchunked.  Both give the same
+    bits, and a graph captured later (chunked, forked onto the plan's streams) replays them."""
+    n = 260
+    sc, layers, weights, convs, x = _chain_setup(n)
+    fin = torch.empty((n,) + convs[-1].out_shape, device=DEV)
+    s = torch.cuda.Stream()
+    outs = [None] * (len(convs) - 1) + [fin]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sc.chain_forward(convs, x, outs, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    captured = fin.clone()
+    fin.zero_()
+    sc.chain_forward(convs, x, outs)  # eager: creates the streams, chunked
+    torch.cuda.synchronize()
+    assert torch.equal(fin, captured)
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=s):
+        sc.chain_forward(convs, x, outs, stream=s)
+    fin.zero_()
+    g2.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(fin, captured)
